@@ -1,0 +1,598 @@
+// Host orchestrator and C ABI of the B200 swept solver.
+//
+// Replaces the reference engine (inc/detail/engines_impl.hpp):
+//   run_decomposed<Model>  :327-415  -> s1d_create + s1d_advance + s1d_read_state
+//   swept_worker<Model>    :234-321  -> run_swept(): Up, (Diamond)*, Down, classic pad
+//   classic_worker<Model>  :201-213  -> run_classic_steps(): one launch per substep
+//   RingTransport::shift / exchange  -> boundary tiles / classic halos read the
+//                                       neighbour shard's buffers directly (peer
+//                                       pointers over NVLink); cross-shard order
+//                                       is enforced with CUDA events, one wait per
+//                                       neighbour per launch.
+// Shard r of the periodic ring lives on device (r % num_devices); the whole
+// stepping loop is asynchronous on one stream per shard, timed with CUDA events.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include <cuda_runtime.h>
+
+#include "host_config.hpp"
+#include "kernels.hpp"
+#include "swept1d.h"
+
+namespace s1d {
+namespace {
+
+struct CudaError : Error {
+    explicit CudaError(const std::string& what) : Error(S1D_CUDA_ERROR, what) {}
+};
+
+#define S1D_CUDA(call)                                                                                   \
+    do {                                                                                                 \
+        cudaError_t e_ = (call);                                                                         \
+        if (e_ != cudaSuccess)                                                                           \
+            throw CudaError(std::string(#call) + ": " + cudaGetErrorString(e_));                          \
+    } while (0)
+
+struct Shard {
+    int dev = 0;
+    cudaStream_t st = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_done = nullptr;
+    std::uint64_t N = 0, nb = 0, start = 0;
+    std::uint64_t fstride = 0; // doubles between SoA fields of a state buffer
+    double* ic = nullptr;      // resident initial state
+    double* state[2] = {nullptr, nullptr};
+    double* EL[2] = {nullptr, nullptr};
+    double* ER[2] = {nullptr, nullptr};
+    int* err = nullptr;
+    const double* final_state = nullptr;
+};
+
+} // namespace
+
+struct Solver {
+    s1d_config cfg{};
+    Spec spec;
+    Partition part;
+    std::vector<Shard> shards;
+    int ndev = 1;
+    std::uint64_t m = 0;
+    int p = 2;
+    double setup_seconds = 0.0;
+    std::string last_error;
+    std::vector<double> host_ic;
+
+    ~Solver() { release(); }
+
+    void release() {
+        for (auto& s : shards) {
+            cudaSetDevice(s.dev);
+            if (s.st) cudaStreamSynchronize(s.st);
+            cudaFree(s.ic);
+            for (int k = 0; k < 2; ++k) {
+                cudaFree(s.state[k]);
+                cudaFree(s.EL[k]);
+                cudaFree(s.ER[k]);
+            }
+            cudaFree(s.err);
+            if (s.ev_start) cudaEventDestroy(s.ev_start);
+            if (s.ev_stop) cudaEventDestroy(s.ev_stop);
+            if (s.ev_done) cudaEventDestroy(s.ev_done);
+            if (s.st) cudaStreamDestroy(s.st);
+        }
+        shards.clear();
+    }
+
+    Shard& left_of(int g) { return shards[static_cast<std::size_t>(part.left[static_cast<std::size_t>(g)])]; }
+    Shard& right_of(int g) { return shards[static_cast<std::size_t>(part.right[static_cast<std::size_t>(g)])]; }
+    int R() const { return static_cast<int>(shards.size()); }
+
+    void init(const s1d_config& in) {
+        const auto t0 = std::chrono::steady_clock::now();
+        cfg = in;
+        finalize(cfg, true);
+        spec = make_spec(cfg.equation, cfg.method);
+        if (cfg.equation != S1D_HEAT)
+            throw Error(S1D_INVALID_CONFIG, "equation not yet supported by the B200 path");
+        part = make_partition(cfg);
+        m = cycle_advance(cfg.block_width, static_cast<std::uint64_t>(spec.h));
+        p = heat_points_per_thread(static_cast<int>(cfg.block_width));
+
+        int visible = 0;
+        if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0)
+            throw Error(S1D_NO_DEVICE, "no CUDA device visible");
+        ndev = cfg.num_devices > 0 ? std::min(cfg.num_devices, visible) : visible;
+        ndev = std::min(ndev, cfg.ranks);
+
+        // Peer access between ring neighbours on distinct devices.
+        for (int g = 0; g < cfg.ranks; ++g) {
+            const int d = g % ndev;
+            for (int nb : {part.left[static_cast<std::size_t>(g)], part.right[static_cast<std::size_t>(g)]}) {
+                const int dn = nb % ndev;
+                if (dn == d) continue;
+                int ok = 0;
+                S1D_CUDA(cudaDeviceCanAccessPeer(&ok, d, dn));
+                if (!ok) throw Error(S1D_PEER_UNAVAILABLE, "device " + std::to_string(d) +
+                                                               " cannot access peer " + std::to_string(dn));
+                S1D_CUDA(cudaSetDevice(d));
+                const cudaError_t e = cudaDeviceEnablePeerAccess(dn, 0);
+                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+                    throw CudaError(std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+                cudaGetLastError();
+            }
+        }
+
+        host_ic = initial_condition(initial_or_default(cfg), cfg.grid_size, cfg.equation, cfg.gamma);
+        const std::uint64_t w = cfg.block_width;
+        shards.resize(static_cast<std::size_t>(cfg.ranks));
+        for (int g = 0; g < cfg.ranks; ++g) {
+            Shard& s = shards[static_cast<std::size_t>(g)];
+            s.dev = g % ndev;
+            s.nb = part.blocks[static_cast<std::size_t>(g)];
+            s.N = s.nb * w;
+            s.start = part.start[static_cast<std::size_t>(g)];
+            s.fstride = s.N;
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+            S1D_CUDA(cudaEventCreate(&s.ev_start));
+            S1D_CUDA(cudaEventCreate(&s.ev_stop));
+            S1D_CUDA(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
+            const std::size_t state_bytes = sizeof(double) * s.N * static_cast<std::size_t>(spec.rec);
+            S1D_CUDA(cudaMalloc(&s.ic, state_bytes));
+            S1D_CUDA(cudaMalloc(&s.state[0], state_bytes));
+            S1D_CUDA(cudaMalloc(&s.state[1], state_bytes));
+            S1D_CUDA(cudaMalloc(&s.err, sizeof(int)));
+            S1D_CUDA(cudaMemset(s.err, 0, sizeof(int)));
+            if (cfg.scheme == S1D_SWEPT) {
+                const std::size_t edge_bytes = sizeof(double) * s.nb * w * static_cast<std::size_t>(spec.rec);
+                for (int k = 0; k < 2; ++k) {
+                    S1D_CUDA(cudaMalloc(&s.EL[k], edge_bytes));
+                    S1D_CUDA(cudaMalloc(&s.ER[k], edge_bytes));
+                }
+            }
+        }
+        upload(host_ic.data());
+        sync_all();
+        setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+
+    void sync_all() {
+        for (auto& s : shards) {
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(cudaStreamSynchronize(s.st));
+        }
+    }
+
+    // Global-order host state (vpp doubles per point) -> per-shard SoA ic.
+    void upload(const double* host) {
+        const int vpp = spec.vpp;
+        for (auto& s : shards) {
+            S1D_CUDA(cudaSetDevice(s.dev));
+            if (vpp == 1) {
+                S1D_CUDA(cudaMemcpyAsync(s.ic, host + s.start, sizeof(double) * s.N, cudaMemcpyHostToDevice, s.st));
+            } else {
+                throw Error(S1D_INTERNAL, "multi-value upload not implemented");
+            }
+        }
+    }
+
+    void download(double* host) {
+        const int vpp = spec.vpp;
+        for (auto& s : shards) {
+            S1D_CUDA(cudaSetDevice(s.dev));
+            if (vpp == 1) {
+                S1D_CUDA(cudaMemcpyAsync(host + s.start, s.final_state, sizeof(double) * s.N,
+                                         cudaMemcpyDeviceToHost, s.st));
+            } else {
+                throw Error(S1D_INTERNAL, "multi-value download not implemented");
+            }
+        }
+        sync_all();
+    }
+
+    // Cross-shard ordering: every launch on shard g waits for the previous
+    // launch of both ring neighbours (RAW on the edges/halos it reads, WAR on
+    // the buffers they read). Waits of a round are enqueued before any event
+    // of the round is re-recorded.
+    void wait_neighbours() {
+        if (R() == 1) return;
+        for (int g = 0; g < R(); ++g) {
+            Shard& s = shards[static_cast<std::size_t>(g)];
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(cudaStreamWaitEvent(s.st, left_of(g).ev_done, 0));
+            S1D_CUDA(cudaStreamWaitEvent(s.st, right_of(g).ev_done, 0));
+        }
+    }
+    void record_round() {
+        if (R() == 1) return;
+        for (auto& s : shards) {
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(cudaEventRecord(s.ev_done, s.st));
+        }
+    }
+
+    void classic_steps(std::int64_t c_begin, std::int64_t c_end, const double** cur_per_shard, int* cur_idx,
+                       s1d_stats& stats) {
+        // cur_per_shard[g]: buffer holding the current level; results ping-pong
+        // through state[0]/state[1] (cur_idx: which one holds the result, -1 = ic).
+        for (std::int64_t c = c_begin; c <= c_end; ++c) {
+            wait_neighbours();
+            const int nxt = (*cur_idx == 0) ? 1 : 0;
+            for (int g = 0; g < R(); ++g) {
+                Shard& s = shards[static_cast<std::size_t>(g)];
+                Shard& L = left_of(g);
+                Shard& Rt = right_of(g);
+                const double* curL = cur_per_shard[part.left[static_cast<std::size_t>(g)]];
+                const double* curR = cur_per_shard[part.right[static_cast<std::size_t>(g)]];
+                ClassicArgs a;
+                a.N = s.N;
+                a.h = spec.h;
+                a.counter = c;
+                a.fstride = s.fstride;
+                a.in = cur_per_shard[g];
+                a.out = s.state[nxt];
+                a.halo_l = curL + (L.N - static_cast<std::uint64_t>(spec.h));
+                a.halo_r = curR;
+                a.halo_l_fstride = L.fstride;
+                a.halo_r_fstride = Rt.fstride;
+                a.fourier = cfg.fourier;
+                a.gamma = cfg.gamma;
+                a.dt_dx = cfg.dt_dx;
+                a.error_flag = s.err;
+                S1D_CUDA(cudaSetDevice(s.dev));
+                S1D_CUDA(launch_heat_classic(a, s.st));
+                stats.kernel_launches += 1;
+            }
+            record_round();
+            *cur_idx = nxt;
+            for (int g = 0; g < R(); ++g) cur_per_shard[g] = shards[static_cast<std::size_t>(g)].state[nxt];
+        }
+    }
+
+    void swept_phase(int kind, std::int64_t j, s1d_stats& stats) {
+        wait_neighbours();
+        const int w = static_cast<int>(cfg.block_width);
+        const int src = static_cast<int>((j + 1) & 1), dst = static_cast<int>(j & 1);
+        for (int g = 0; g < R(); ++g) {
+            Shard& s = shards[static_cast<std::size_t>(g)];
+            Shard& L = left_of(g);
+            Shard& Rt = right_of(g);
+            TileArgs a;
+            a.w = w;
+            a.h = spec.h;
+            a.m = static_cast<int>(m);
+            a.nb = static_cast<int>(s.nb);
+            a.seam = (kind == kUp) ? 0 : static_cast<int>(j & 1);
+            a.p = p;
+            a.base = (kind == kUp) ? -static_cast<std::int64_t>(m) : (j - 1) * static_cast<std::int64_t>(m);
+            a.N = s.N;
+            a.rec = spec.rec;
+            a.fstride = s.fstride;
+            a.state_in = s.ic;
+            a.state_out = s.state[0];
+            a.state_right = Rt.state[0];
+            a.right_fstride = Rt.fstride;
+            a.in_R = s.ER[src];
+            a.in_L = s.EL[src];
+            a.peer_R = L.ER[src] + (L.nb - 1) * static_cast<std::uint64_t>(w) * static_cast<std::uint64_t>(spec.rec);
+            a.peer_L = Rt.EL[src];
+            a.out_L = s.EL[dst];
+            a.out_R = s.ER[dst];
+            a.fourier = cfg.fourier;
+            a.gamma = cfg.gamma;
+            a.dt_dx = cfg.dt_dx;
+            a.error_flag = s.err;
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(launch_heat_tile(kind, a, s.st));
+            stats.kernel_launches += 1;
+            if (R() > 1 && kind != kUp)
+                stats.edge_bytes_device += sizeof(double) * static_cast<std::uint64_t>(w) * spec.rec;
+        }
+        record_round();
+    }
+
+    void advance(s1d_stats* stats_out, s1d_timing* timing_out) {
+        s1d_stats stats{};
+        const std::int64_t total = cfg.steps * spec.S;
+        const std::int64_t cycles = cfg.scheme == S1D_SWEPT ? total / static_cast<std::int64_t>(m) : 0;
+        const std::int64_t pad = total - cycles * static_cast<std::int64_t>(m);
+
+        sync_all();
+        for (auto& s : shards) {
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(cudaMemsetAsync(s.err, 0, sizeof(int), s.st));
+            S1D_CUDA(cudaEventRecord(s.ev_start, s.st));
+        }
+        record_round();
+
+        std::vector<const double*> cur(static_cast<std::size_t>(R()));
+        int cur_idx = -1;
+        for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].ic;
+        if (cycles >= 1) {
+            swept_phase(kUp, 0, stats);
+            for (std::int64_t j = 1; j <= cycles; ++j) swept_phase(j == cycles ? kDown : kDiamond, j, stats);
+            cur_idx = 0;
+            for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].state[0];
+        }
+        if (pad > 0) classic_steps(cycles * static_cast<std::int64_t>(m) + 1, total, cur.data(), &cur_idx, stats);
+
+        for (auto& s : shards) {
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(cudaEventRecord(s.ev_stop, s.st));
+        }
+        sync_all();
+        float worst_ms = 0.0f;
+        int flag = 0;
+        for (int g = 0; g < R(); ++g) {
+            Shard& s = shards[static_cast<std::size_t>(g)];
+            S1D_CUDA(cudaSetDevice(s.dev));
+            float ms = 0.0f;
+            S1D_CUDA(cudaEventElapsedTime(&ms, s.ev_start, s.ev_stop));
+            worst_ms = std::max(worst_ms, ms);
+            int f = 0;
+            S1D_CUDA(cudaMemcpy(&f, s.err, sizeof(int), cudaMemcpyDeviceToHost));
+            flag |= f;
+            s.final_state = cur[static_cast<std::size_t>(g)];
+        }
+        S1D_CUDA(cudaGetLastError());
+        if (flag) throw Error(S1D_NONPHYSICAL, "non-physical state encountered on the device");
+
+        // Reference accounting (transport.cpp:48-110): a swept cycle is one
+        // shift round (1 message of (w/2+h) records per rank); a classic or
+        // pad substep is one exchange round (2 messages of h records).
+        const std::uint64_t Rn = static_cast<std::uint64_t>(R());
+        const std::uint64_t cell = sizeof(double) * static_cast<std::uint64_t>(spec.slots);
+        const std::uint64_t buf = cfg.block_width / 2 + static_cast<std::uint64_t>(spec.h);
+        stats.exchange_rounds = static_cast<std::uint64_t>(cycles + pad);
+        stats.messages_sent = Rn * static_cast<std::uint64_t>(cycles + 2 * pad);
+        stats.bytes_sent = Rn * (static_cast<std::uint64_t>(cycles) * buf * cell +
+                                 static_cast<std::uint64_t>(pad) * 2 * static_cast<std::uint64_t>(spec.h) * cell);
+        if (Rn > 1)
+            stats.edge_bytes_device += static_cast<std::uint64_t>(pad) * Rn * 2 * sizeof(double) *
+                                       static_cast<std::uint64_t>(spec.h) * static_cast<std::uint64_t>(spec.rec);
+        if (stats_out) *stats_out = stats;
+        if (timing_out) {
+            timing_out->setup_seconds = setup_seconds;
+            timing_out->loop_seconds = worst_ms * 1e-3;
+            timing_out->virtual_seconds = 0.0;
+        }
+    }
+
+    std::size_t state_len() const { return cfg.grid_size * static_cast<std::uint64_t>(spec.vpp); }
+};
+
+} // namespace s1d
+
+// ---------------------------------------------------------------------------
+// C ABI
+// ---------------------------------------------------------------------------
+struct s1d_solver {
+    s1d::Solver impl;
+};
+
+namespace {
+
+void put_err(char* err, size_t errlen, const std::string& what) {
+    if (!err || errlen == 0) return;
+    const size_t n = std::min(errlen - 1, what.size());
+    std::memcpy(err, what.data(), n);
+    err[n] = '\0';
+}
+
+template <class Fn>
+int guarded(char* err, size_t errlen, Fn&& fn) {
+    try {
+        fn();
+        put_err(err, errlen, "");
+        return S1D_OK;
+    } catch (const s1d::Error& e) {
+        put_err(err, errlen, e.what());
+        return e.status;
+    } catch (const std::exception& e) {
+        put_err(err, errlen, e.what());
+        return S1D_INTERNAL;
+    }
+}
+
+template <class Fn>
+int guarded_solver(s1d_solver* s, Fn&& fn) {
+    char buf[512];
+    const int st = guarded(buf, sizeof buf, fn);
+    if (s) s->impl.last_error = buf;
+    return st;
+}
+
+} // namespace
+
+extern "C" {
+
+const char* s1d_version(void) { return "swept1d-b200 0.1.0 (sm_100a, FP64)"; }
+int s1d_abi_version(void) { return S1D_ABI_VERSION; }
+
+int s1d_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+void s1d_config_defaults(s1d_config* c) {
+    std::memset(c, 0, sizeof(*c));
+    c->equation = S1D_HEAT;
+    c->method = S1D_LENGTHENING;
+    c->scheme = S1D_SWEPT;
+    c->mode = S1D_VIRTUAL;
+    c->grid_size = 1024;
+    c->block_width = 32;
+    c->ranks = 2;
+    c->work_factor = 0;
+    c->steps = 50;
+    c->fourier = 0.4;
+    c->gamma = 1.4;
+    c->dt_dx = 0.0;
+    c->cfl = 0.4;
+    c->alpha = 0.0;
+    c->beta = 0.0;
+    c->compute_cost = 1e-8;
+    c->num_devices = 0;
+}
+
+int s1d_apply_config_entry(s1d_config* cfg, const char* key, const char* value, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { s1d::apply_config_entry(*cfg, key, value); });
+}
+
+int s1d_validate(const s1d_config* cfg, int partitioned, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { s1d::validate(*cfg, partitioned != 0); });
+}
+
+int s1d_finalize(s1d_config* cfg, int partitioned, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { s1d::finalize(*cfg, partitioned != 0); });
+}
+
+void s1d_spec(int equation, int method, int* substeps, int* half_width, int* slots, int* vpp) {
+    const s1d::Spec s = s1d::make_spec(equation, method);
+    if (substeps) *substeps = s.S;
+    if (half_width) *half_width = s.h;
+    if (slots) *slots = s.slots;
+    if (vpp) *vpp = s.vpp;
+}
+
+int s1d_initial_condition(const char* id, uint64_t n, int equation, double gamma, double* out, size_t out_len,
+                          char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const auto v = s1d::initial_condition(id, n, equation, gamma);
+        if (v.size() > out_len) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
+int s1d_max_signal_speed(const double* prim, size_t len, double gamma, double* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] { *out = s1d::max_signal_speed(prim, len, gamma); });
+}
+
+int s1d_partition(const s1d_config* cfg, uint64_t* blocks, uint64_t* start, int* left, int* right, char* err,
+                  size_t errlen) {
+    return guarded(err, errlen, [&] {
+        const auto p = s1d::make_partition(*cfg);
+        for (std::size_t r = 0; r < p.blocks.size(); ++r) {
+            blocks[r] = p.blocks[r];
+            start[r] = p.start[r];
+            left[r] = p.left[r];
+            right[r] = p.right[r];
+        }
+    });
+}
+
+int64_t s1d_cycle_advance(uint64_t w, uint64_t h, char* err, size_t errlen) {
+    std::uint64_t m = 0;
+    const int st = guarded(err, errlen, [&] { m = s1d::cycle_advance(w, h); });
+    return st == S1D_OK ? static_cast<int64_t>(m) : -st;
+}
+
+int64_t s1d_schedule(int kind, uint64_t w, uint64_t h, int64_t* substep, int64_t* lo, int64_t* hi, size_t cap,
+                     char* err, size_t errlen) {
+    std::vector<s1d::Level> lv;
+    const int st = guarded(err, errlen, [&] { lv = s1d::schedule(kind, w, h); });
+    if (st != S1D_OK) return -st;
+    for (std::size_t i = 0; i < lv.size() && i < cap; ++i) {
+        substep[i] = lv[i].substep;
+        lo[i] = lv[i].lo;
+        hi[i] = lv[i].hi;
+    }
+    return static_cast<int64_t>(lv.size());
+}
+
+uint64_t s1d_swept_buffer_cells(uint64_t w, int equation, int method) {
+    return w / 2 + static_cast<uint64_t>(s1d::make_spec(equation, method).h);
+}
+
+int s1d_create(const s1d_config* cfg, s1d_solver** out, char* err, size_t errlen) {
+    *out = nullptr;
+    auto holder = std::make_unique<s1d_solver>();
+    const int st = guarded(err, errlen, [&] { holder->impl.init(*cfg); });
+    if (st == S1D_OK) *out = holder.release();
+    return st;
+}
+
+void s1d_destroy(s1d_solver* s) { delete s; }
+
+int s1d_get_config(const s1d_solver* s, s1d_config* out) {
+    *out = s->impl.cfg;
+    return S1D_OK;
+}
+
+int s1d_set_initial(s1d_solver* s, const double* host_state, size_t len) {
+    return guarded_solver(s, [&] {
+        if (!host_state) {
+            s->impl.upload(s->impl.host_ic.data());
+        } else {
+            if (len != s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "initial state length mismatch");
+            s->impl.upload(host_state);
+        }
+        s->impl.sync_all();
+    });
+}
+
+int s1d_advance(s1d_solver* s, s1d_stats* stats, s1d_timing* timing) {
+    return guarded_solver(s, [&] {
+        if (timing) std::memset(timing, 0, sizeof(*timing));
+        s->impl.advance(stats, timing);
+    });
+}
+
+int s1d_read_state(s1d_solver* s, double* host_out, size_t len) {
+    return guarded_solver(s, [&] {
+        if (len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
+        for (auto& sh : s->impl.shards)
+            if (!sh.final_state) throw s1d::Error(S1D_INVALID_CONFIG, "no state: call s1d_advance first");
+        s->impl.download(host_out);
+    });
+}
+
+int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_out, size_t out_len,
+              s1d_stats* stats, s1d_timing* timing) {
+    return guarded_solver(s, [&] {
+        if (host_in && in_len != s->impl.state_len())
+            throw s1d::Error(S1D_INVALID_CONFIG, "initial state length mismatch");
+        if (out_len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
+        s1d_timing t{};
+        const auto t0 = std::chrono::steady_clock::now();
+        s->impl.upload(host_in ? host_in : s->impl.host_ic.data());
+        s->impl.sync_all();
+        const auto t1 = std::chrono::steady_clock::now();
+        s->impl.advance(stats, &t);
+        const auto t2 = std::chrono::steady_clock::now();
+        s->impl.download(host_out);
+        const auto t3 = std::chrono::steady_clock::now();
+        t.h2d_seconds = std::chrono::duration<double>(t1 - t0).count();
+        t.d2h_seconds = std::chrono::duration<double>(t3 - t2).count();
+        if (timing) *timing = t;
+    });
+}
+
+const char* s1d_last_error(const s1d_solver* s) { return s ? s->impl.last_error.c_str() : ""; }
+
+int s1d_run(const s1d_config* cfg, double* state_out, size_t state_len, s1d_stats* stats, s1d_timing* timing,
+            char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        s1d::Solver solver;
+        solver.init(*cfg);
+        if (state_len < solver.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
+        s1d_timing t{};
+        solver.advance(stats, &t);
+        const auto t2 = std::chrono::steady_clock::now();
+        solver.download(state_out);
+        t.d2h_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
+        if (timing) *timing = t;
+    });
+}
+
+} // extern "C"

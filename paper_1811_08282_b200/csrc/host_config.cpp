@@ -1,0 +1,240 @@
+// Host-side configuration, geometry and initial conditions (see
+// host_config.hpp for the reference file:line each function follows).
+#include "host_config.hpp"
+
+#include <algorithm>
+#include <cctype>
+#include <cmath>
+#include <cstring>
+
+namespace s1d {
+
+Spec make_spec(int equation, int method) {
+    Spec s;
+    if (equation == S1D_HEAT) {
+        s = Spec{1, 1, 2, 1, 1};
+    } else if (method == S1D_LENGTHENING) {
+        s = Spec{4, 1, 7, 3, 7};
+    } else {
+        s = Spec{2, 2, 6, 3, 6};
+    }
+    return s;
+}
+
+std::string initial_or_default(const s1d_config& cfg) {
+    const std::size_t len = strnlen(cfg.initial, sizeof(cfg.initial));
+    if (len) return std::string(cfg.initial, len);
+    return cfg.equation == S1D_HEAT ? "heat-sine" : "euler-sod-periodic";
+}
+
+static std::string num(double v) { return std::to_string(v); }
+static std::string num(std::uint64_t v) { return std::to_string(v); }
+static std::string num(std::int64_t v) { return std::to_string(v); }
+static std::string num(int v) { return std::to_string(v); }
+
+void validate(const s1d_config& cfg, bool partitioned) {
+    if (cfg.equation != S1D_HEAT && cfg.equation != S1D_EULER)
+        throw Error(S1D_INVALID_CONFIG, "unknown equation (expected heat|euler)");
+    if (cfg.method != S1D_LENGTHENING && cfg.method != S1D_FLATTENING)
+        throw Error(S1D_INVALID_CONFIG, "unknown method (expected lengthening|flattening)");
+    if (cfg.scheme != S1D_CLASSIC && cfg.scheme != S1D_SWEPT)
+        throw Error(S1D_INVALID_CONFIG, "unknown scheme (expected classic|swept)");
+    const Spec s = make_spec(cfg.equation, cfg.method);
+    const std::uint64_t h = static_cast<std::uint64_t>(s.h);
+    if (cfg.grid_size < 2 * h + 1)
+        throw Error(S1D_INVALID_CONFIG, "grid size " + num(cfg.grid_size) + " is too small for the stencil");
+    if (cfg.steps < 0) throw Error(S1D_INVALID_CONFIG, "step count must be >= 0, got " + num(cfg.steps));
+    if (!(cfg.fourier > 0.0) || cfg.fourier > 0.5)
+        throw Error(S1D_INVALID_CONFIG, "Fourier number must lie in (0, 0.5], got " + num(cfg.fourier));
+    if (!(cfg.gamma > 1.0)) throw Error(S1D_INVALID_CONFIG, "gamma must exceed 1, got " + num(cfg.gamma));
+    if (cfg.alpha < 0.0 || cfg.beta < 0.0 || cfg.compute_cost < 0.0)
+        throw Error(S1D_INVALID_CONFIG, "transport cost parameters must be non-negative");
+    if (!partitioned) return;
+
+    const std::uint64_t w = cfg.block_width;
+    if (w < 4 || (w & 1))
+        throw Error(S1D_INVALID_CONFIG, "block width must be even and >= 4, got " + num(w));
+    if (w < 4 * h)
+        throw Error(S1D_INVALID_CONFIG, "block width " + num(w) + " must be >= 4*h = " + num(4 * h) +
+                                            " for stencil half-width " + num(h));
+    if (w % (2 * h) != 0)
+        throw Error(S1D_INVALID_CONFIG, "block width " + num(w) + " must be a multiple of 2*h = " + num(2 * h));
+    // Deviation (documented in DESIGN.md): the reference demands >= 2 ranks
+    // (config.cpp:79-81); one GPU is a valid ring of one shard here.
+    if (cfg.ranks < 1) throw Error(S1D_INVALID_CONFIG, "rank count must be >= 1, got " + num(cfg.ranks));
+    if (cfg.work_factor < 0)
+        throw Error(S1D_INVALID_CONFIG, "work factor must be >= 0, got " + num(cfg.work_factor));
+    if (cfg.grid_size % w != 0)
+        throw Error(S1D_INVALID_CONFIG,
+                    "grid size " + num(cfg.grid_size) + " is not divisible by block width " + num(w));
+    const std::uint64_t total_blocks = cfg.grid_size / w;
+    const std::uint64_t shares =
+        static_cast<std::uint64_t>(cfg.work_factor > 0 ? cfg.ranks - 1 + cfg.work_factor : cfg.ranks);
+    if (total_blocks % shares != 0)
+        throw Error(S1D_INVALID_CONFIG, "total blocks " + num(total_blocks) +
+                                            " not divisible by shares (R-1+WF or R) = " + num(shares));
+}
+
+void finalize(s1d_config& cfg, bool partitioned) {
+    validate(cfg, partitioned);
+    if (cfg.equation == S1D_EULER && cfg.dt_dx == 0.0) {
+        const auto ic = initial_condition(initial_or_default(cfg), cfg.grid_size, cfg.equation, cfg.gamma);
+        cfg.dt_dx = cfg.cfl / max_signal_speed(ic.data(), ic.size(), cfg.gamma);
+    }
+}
+
+void apply_config_entry(s1d_config& cfg, const std::string& key, const std::string& value) {
+    auto to_u = [&](const std::string& v) { return static_cast<std::uint64_t>(std::stoull(v)); };
+    try {
+        if (key == "equation") {
+            if (value == "heat") cfg.equation = S1D_HEAT;
+            else if (value == "euler") cfg.equation = S1D_EULER;
+            else throw Error(S1D_INVALID_CONFIG, "unknown equation '" + value + "' (expected heat|euler)");
+        } else if (key == "method") {
+            if (value == "lengthening") cfg.method = S1D_LENGTHENING;
+            else if (value == "flattening") cfg.method = S1D_FLATTENING;
+            else throw Error(S1D_INVALID_CONFIG,
+                             "unknown method '" + value + "' (expected lengthening|flattening)");
+        } else if (key == "scheme") {
+            if (value == "classic") cfg.scheme = S1D_CLASSIC;
+            else if (value == "swept") cfg.scheme = S1D_SWEPT;
+            else throw Error(S1D_INVALID_CONFIG, "unknown scheme '" + value + "' (expected classic|swept)");
+        } else if (key == "mode") {
+            if (value == "wall") cfg.mode = S1D_WALL;
+            else if (value == "virtual") cfg.mode = S1D_VIRTUAL;
+            else throw Error(S1D_INVALID_CONFIG, "unknown mode '" + value + "' (expected wall|virtual)");
+        } else if (key == "n" || key == "grid_size") cfg.grid_size = to_u(value);
+        else if (key == "w" || key == "block_width") cfg.block_width = to_u(value);
+        else if (key == "ranks") cfg.ranks = std::stoi(value);
+        else if (key == "wf" || key == "work_factor") cfg.work_factor = std::stoi(value);
+        else if (key == "steps") cfg.steps = std::stoll(value);
+        else if (key == "initial") {
+            if (value.size() >= sizeof(cfg.initial))
+                throw Error(S1D_INVALID_CONFIG, "initial condition id too long");
+            std::memset(cfg.initial, 0, sizeof(cfg.initial));
+            std::memcpy(cfg.initial, value.data(), value.size());
+        } else if (key == "fourier") cfg.fourier = std::stod(value);
+        else if (key == "gamma") cfg.gamma = std::stod(value);
+        else if (key == "cfl") cfg.cfl = std::stod(value);
+        else if (key == "alpha") cfg.alpha = std::stod(value);
+        else if (key == "beta") cfg.beta = std::stod(value);
+        else if (key == "compute_cost") cfg.compute_cost = std::stod(value);
+        else if (key == "num_devices") cfg.num_devices = std::stoi(value);
+        else throw Error(S1D_INVALID_CONFIG, "unknown config key '" + key + "'");
+    } catch (const std::invalid_argument&) {
+        throw Error(S1D_INVALID_CONFIG, "bad value '" + value + "' for key '" + key + "'");
+    } catch (const std::out_of_range&) {
+        throw Error(S1D_INVALID_CONFIG, "value '" + value + "' out of range for key '" + key + "'");
+    }
+}
+
+// sin(2*pi*j/n) with quarter-wave folding (partition.cpp:54-63): exact zeros
+// and +-1 at the symmetry points. Uses the host libm sin so values are the
+// reference's bit for bit.
+static double sine_sample(std::uint64_t j, std::uint64_t n) {
+    std::uint64_t k = j % n;
+    double sign = 1.0;
+    if (2 * k >= n) {
+        sign = -1.0;
+        k -= n / 2;
+    }
+    const std::uint64_t folded = (4 * k > n) ? (n / 2 - k) : k;
+    return sign * std::sin(2.0 * M_PI * static_cast<double>(folded) / static_cast<double>(n));
+}
+
+std::vector<double> initial_condition(const std::string& id, std::uint64_t n, int equation, double gamma) {
+    std::vector<double> out;
+    if (equation == S1D_HEAT) {
+        out.resize(n);
+        if (id == "heat-sine") {
+            for (std::uint64_t j = 0; j < n; ++j) out[j] = sine_sample(j, n);
+        } else if (id == "uniform") {
+            std::fill(out.begin(), out.end(), 1.0);
+        } else {
+            throw Error(S1D_UNKNOWN_IC, "initial condition '" + id + "' unknown for heat");
+        }
+        return out;
+    }
+    const bool sod = id == "euler-sod-periodic";
+    if (!sod && id != "uniform") throw Error(S1D_UNKNOWN_IC, "initial condition '" + id + "' unknown for euler");
+    out.resize(3 * n);
+    for (std::uint64_t j = 0; j < n; ++j) {
+        const bool right = sod && !(2 * j < n);
+        const double rho = right ? 0.125 : 1.0, u = 0.0, p = right ? 0.1 : 1.0;
+        out[3 * j] = rho;
+        out[3 * j + 1] = rho * u;
+        out[3 * j + 2] = p / (gamma - 1.0) + 0.5 * rho * u * u;
+    }
+    return out;
+}
+
+static double host_pressure(double rho, double mom, double ene, double gamma) {
+    if (!(rho > 0.0)) throw Error(S1D_NONPHYSICAL, "pressure: non-positive density " + num(rho));
+    const double p = (gamma - 1.0) * (ene - 0.5 * mom * mom / rho);
+    if (!(p > 0.0)) throw Error(S1D_NONPHYSICAL, "pressure: non-positive pressure " + num(p));
+    return p;
+}
+
+double max_signal_speed(const double* prim, std::size_t len, double gamma) {
+    double best = 0.0;
+    for (std::size_t j = 0; j + 2 < len; j += 3) {
+        const double p = host_pressure(prim[j], prim[j + 1], prim[j + 2], gamma);
+        const double u = prim[j + 1] / prim[j];
+        best = std::max(best, std::abs(u) + std::sqrt(gamma * p / prim[j]));
+    }
+    return best;
+}
+
+Partition make_partition(const s1d_config& cfg) {
+    validate(cfg, true);
+    Partition p;
+    const int r = cfg.ranks;
+    const std::uint64_t total_blocks = cfg.grid_size / cfg.block_width;
+    const std::uint64_t shares = static_cast<std::uint64_t>(cfg.work_factor > 0 ? r - 1 + cfg.work_factor : r);
+    const std::uint64_t per_share = total_blocks / shares;
+    p.blocks.assign(static_cast<std::size_t>(r), per_share);
+    if (cfg.work_factor > 0) p.blocks[0] = per_share * static_cast<std::uint64_t>(cfg.work_factor);
+    p.start.resize(static_cast<std::size_t>(r));
+    p.left.resize(static_cast<std::size_t>(r));
+    p.right.resize(static_cast<std::size_t>(r));
+    std::uint64_t start = 0;
+    for (int i = 0; i < r; ++i) {
+        p.start[static_cast<std::size_t>(i)] = start;
+        start += p.blocks[static_cast<std::size_t>(i)] * cfg.block_width;
+        p.left[static_cast<std::size_t>(i)] = (i + r - 1) % r;
+        p.right[static_cast<std::size_t>(i)] = (i + 1) % r;
+    }
+    return p;
+}
+
+static void check_width(std::uint64_t w, std::uint64_t h) {
+    if (h < 1) throw Error(S1D_INVALID_WIDTH, "stencil half-width must be >= 1");
+    if (w < 4 || (w & 1) || w < 4 * h || w % (2 * h) != 0)
+        throw Error(S1D_INVALID_WIDTH, "block width " + num(w) +
+                                           " must be even, >= 4*h and a multiple of 2*h for half-width " + num(h));
+}
+
+std::uint64_t cycle_advance(std::uint64_t w, std::uint64_t h) {
+    check_width(w, h);
+    return w / (2 * h);
+}
+
+std::vector<Level> schedule(int kind, std::uint64_t w, std::uint64_t h) {
+    check_width(w, h);
+    const std::int64_t m = static_cast<std::int64_t>(w / (2 * h));
+    const std::int64_t hh = static_cast<std::int64_t>(h), ww = static_cast<std::int64_t>(w);
+    std::vector<Level> out;
+    if (kind == 0) {
+        for (std::int64_t k = 1; k < m; ++k) out.push_back({k, k * hh, ww - k * hh});
+    } else if (kind == 1) {
+        for (std::int64_t r = 1; r <= 2 * m - 1; ++r) {
+            const std::int64_t half = hh * std::min(r, 2 * m - r);
+            out.push_back({r, -half, half});
+        }
+    } else {
+        for (std::int64_t r = 1; r <= m; ++r) out.push_back({r, -hh * r, hh * r});
+    }
+    return out;
+}
+
+} // namespace s1d

@@ -1,0 +1,55 @@
+// Host-side configuration, geometry and initial conditions of the swept
+// solver (no CUDA). Restated from the reference's semantics:
+//   LaunchConfig::validate/finalize   src/config.cpp:45-103
+//   make_partition / extents / IC     src/partition.cpp:10-113
+//   cycle_advance / schedules         src/swept.cpp:11-64
+// Errors are thrown as s1d::Error{status, message} and converted to status
+// codes at the C ABI (capi.cpp).
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "swept1d.h"
+
+namespace s1d {
+
+struct Error : std::runtime_error {
+    int status;
+    Error(int st, const std::string& what) : std::runtime_error(what), status(st) {}
+};
+
+struct Spec {
+    int S = 1;     // substeps per time step
+    int h = 1;     // stencil half width
+    int slots = 2; // doubles per reference record
+    int vpp = 1;   // values per point in the output
+    int rec = 1;   // doubles per B200 edge record (full live snapshot)
+};
+
+Spec make_spec(int equation, int method);
+
+std::string initial_or_default(const s1d_config& cfg);
+void validate(const s1d_config& cfg, bool partitioned);
+void finalize(s1d_config& cfg, bool partitioned);
+void apply_config_entry(s1d_config& cfg, const std::string& key, const std::string& value);
+
+std::vector<double> initial_condition(const std::string& id, std::uint64_t n, int equation, double gamma);
+double max_signal_speed(const double* prim, std::size_t len, double gamma);
+
+struct Partition {
+    std::vector<std::uint64_t> blocks, start;
+    std::vector<int> left, right;
+};
+Partition make_partition(const s1d_config& cfg);
+
+std::uint64_t cycle_advance(std::uint64_t w, std::uint64_t h);
+
+struct Level {
+    std::int64_t substep, lo, hi;
+};
+std::vector<Level> schedule(int kind, std::uint64_t w, std::uint64_t h);
+
+} // namespace s1d

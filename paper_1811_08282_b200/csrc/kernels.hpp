@@ -1,0 +1,62 @@
+// Launch interface between the host orchestrator (engine.cu) and the sm_100a
+// kernels (heat.cu, euler.cu). Plain structs of device pointers; no torch.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace s1d {
+
+enum TileKind : int { kUp = 0, kDiamond = 1, kDown = 2 };
+
+// One swept phase over the tiles of a shard.
+// Local tile coordinates x in [0, w+2h) map to shard position
+// g = centre - w/2 - h + x. Registers hold x in [h, w+h).
+struct TileArgs {
+    int w = 0, h = 1, m = 0;  // block width, half width, levels per half cycle
+    int nb = 0;               // tiles in this launch (= blocks of the shard)
+    int seam = 0;             // 1: centres at (b+1)w (odd cycles); 0: bw + w/2
+    int p = 2;                // points per thread
+    std::int64_t base = 0;    // counter of level r is base + r
+    std::uint64_t N = 0;      // shard points
+    int rec = 1;              // doubles per record (per field block)
+    std::uint64_t fstride = 0; // state field stride (doubles) for SoA records
+    // Up: state_in (shard-local, positions [bw, bw+w)); Down: state_out
+    // (positions >= N spill to state_right, the right shard's array).
+    const double* state_in = nullptr;
+    double* state_out = nullptr;
+    double* state_right = nullptr;
+    std::uint64_t right_fstride = 0;
+    // Edges: per tile w records per side, laid out [tile][level][2h][rec].
+    const double* in_R = nullptr;   // producers' right edges (own shard)
+    const double* in_L = nullptr;   // producers' left edges (own shard)
+    const double* peer_R = nullptr; // left shard's last tile R edges (center phase, tile 0)
+    const double* peer_L = nullptr; // right shard's tile 0 L edges (seam phase, last tile)
+    double* out_L = nullptr;
+    double* out_R = nullptr;
+    // physics
+    double fourier = 0.4, gamma = 1.4, dt_dx = 0.0;
+    int* error_flag = nullptr;      // device NonPhysicalState flag (Euler)
+};
+
+struct ClassicArgs {
+    std::uint64_t N = 0;
+    int h = 1;
+    std::int64_t counter = 1;
+    std::uint64_t fstride = 0;
+    const double* in = nullptr;     // SoA fields, stride fstride
+    double* out = nullptr;
+    // halo sources: h records left of position 0 and right of N-1 (possibly
+    // on a peer device), field stride halo_*_fstride.
+    const double* halo_l = nullptr;
+    const double* halo_r = nullptr;
+    std::uint64_t halo_l_fstride = 0, halo_r_fstride = 0;
+    double fourier = 0.4, gamma = 1.4, dt_dx = 0.0;
+    int* error_flag = nullptr;
+};
+
+cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st);
+cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st);
+int heat_points_per_thread(int w);
+
+} // namespace s1d

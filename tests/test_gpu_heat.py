@@ -1,0 +1,96 @@
+"""GPU parity: heat (FTCS) classic and swept vs the CPU oracle, bitwise.
+
+Mirrors test_decomp.cpp:81-145 (classic/swept == serial bitwise) and the
+survey's fingerprints on the B200 path. All calls go through
+the C ABI (libswept1d.so) via the Python mirror.
+"""
+import numpy as np
+import pytest
+
+import paper_1811_08282_b200 as s1d
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def cfg(scheme, n, w, steps, ranks=1, wf=0, **kw):
+    return s1d.LaunchConfig(equation=s1d.Equation.Heat, scheme=scheme, grid_size=n, block_width=w, ranks=ranks,
+                            work_factor=wf, steps=steps, **kw)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def assert_bitwise(got, want):
+    assert got.shape == want.shape
+    bad = np.nonzero(bits(got) != bits(want))[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:8]}: got {got[bad[:4]]} want {want[bad[:4]]}"
+
+
+@pytest.mark.parametrize("scheme", [s1d.Scheme.Swept, s1d.Scheme.Classic])
+@pytest.mark.parametrize("steps,fnv", [(64, "4185347ae18fab0f"), (1000, "90d783358019c683")])
+def test_fingerprint_n16k_w64(gpu, scheme, steps, fnv):
+    res = s1d.run(cfg(scheme, 1 << 14, 64, steps))
+    assert O.fnv1a64(res.state) == fnv
+
+
+# test_decomp.cpp:108-112 heat rows (n, w, ranks, wf, steps)
+DECOMP = [(64, 4, 2, 0, 16), (32, 8, 2, 0, 4), (128, 8, 3, 2, 25), (64, 8, 2, 0, 21)]
+
+
+@pytest.mark.parametrize("n,w,ranks,wf,steps", DECOMP)
+@pytest.mark.parametrize("scheme", [s1d.Scheme.Swept, s1d.Scheme.Classic])
+def test_decomp_cases(gpu, n, w, ranks, wf, steps, scheme):
+    want = O.port_run_serial("heat", n=n, steps=steps)
+    for r in (ranks, 1):
+        got = s1d.run(cfg(scheme, n, w, steps, ranks=r, wf=wf if r > 1 else 0)).state
+        assert_bitwise(got, want)
+
+
+@pytest.mark.parametrize("w", [4, 6, 8, 12, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
+def test_width_sweep_unaligned(gpu, w):
+    n = max(4 * w, 1 << 13)
+    n -= n % w
+    m = w // 2
+    for steps in (m - 1, m, 2 * m, 3 * m + 5, 5 * m + 1):
+        want = O.port_run_serial("heat", n=n, steps=steps)
+        got = s1d.run(cfg(s1d.Scheme.Swept, n, w, steps)).state
+        assert_bitwise(got, want)
+
+
+def test_zero_steps_returns_ic(gpu):
+    for scheme in (s1d.Scheme.Swept, s1d.Scheme.Classic):
+        res = s1d.run(cfg(scheme, 64, 8, 0))
+        ic = s1d.initial_condition("heat-sine", 64, s1d.make_spec(s1d.Equation.Heat, s1d.Method.Lengthening))
+        assert_bitwise(res.state, ic)
+        assert res.stats.exchange_rounds == 0
+
+
+def test_round_counts(gpu):
+    # test_decomp.cpp:147-157, 191-199
+    assert s1d.run(cfg(s1d.Scheme.Swept, 64, 8, 40, ranks=2)).stats.exchange_rounds == 10
+    assert s1d.run(cfg(s1d.Scheme.Classic, 64, 8, 40, ranks=2)).stats.exchange_rounds == 40
+    res = s1d.run(cfg(s1d.Scheme.Swept, 128, 32, 50, ranks=2))
+    assert res.stats.exchange_rounds == 5
+    assert_bitwise(res.state, O.port_run_serial("heat", n=128, steps=50))
+
+
+def test_uniform_fixed_point(gpu):
+    res = s1d.run(cfg(s1d.Scheme.Swept, 256, 16, 37, initial="uniform"))
+    assert np.all(res.state == 1.0)
+
+
+def test_solver_handle_repeat_and_custom_state(gpu):
+    c = cfg(s1d.Scheme.Swept, 1 << 12, 64, 100)
+    with s1d.Solver(c) as sv:
+        a, _, _ = sv.solve()
+        b, _, t = sv.solve()
+        assert_bitwise(a, b)
+        assert t.loop_seconds > 0
+        x = np.random.default_rng(1).standard_normal(1 << 12)
+        got, _, _ = sv.solve(x)
+        # classic on the same input
+    with s1d.Solver(cfg(s1d.Scheme.Classic, 1 << 12, 64, 100)) as sc:
+        want, _, _ = sc.solve(x)
+    assert_bitwise(got, want)
