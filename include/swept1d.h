@@ -112,6 +112,13 @@ typedef struct s1d_timing {
     double virtual_seconds; /* always 0 */
     double h2d_seconds;
     double d2h_seconds;
+    /* The dominant kernel of the run (swept: the Diamond phases; classic: the
+     * per-substep kernel), timed with CUDA events on its own stream around the
+     * contiguous run of those launches (max over shards). */
+    double dominant_seconds;
+    uint64_t dominant_launches;
+    uint64_t dominant_point_updates; /* point-substeps those launches computed (all shards) */
+    char dominant_kernel[32];
 } s1d_timing;
 
 /* ---- library ------------------------------------------------------------ */
@@ -165,6 +172,12 @@ int s1d_read_state(s1d_solver* s, double* host_out, size_t len);
 int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_out, size_t out_len,
               s1d_stats* stats, s1d_timing* timing);
 const char* s1d_last_error(const s1d_solver* s);
+
+/* ---- measurement helpers (not part of the reference interface) --------- */
+/* Sustained FP64 DADD/DMUL instruction rate of `device` (ops/s), measured by
+ * a dependent-chain-free microkernel: the roofline denominator for the
+ * FP64-pipe-bound swept kernels. */
+int s1d_measure_fp64_peak(int device, double* ops_per_second, char* err, size_t errlen);
 
 #ifdef __cplusplus
 }

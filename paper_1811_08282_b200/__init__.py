@@ -10,5 +10,5 @@ from .api import (  # noqa: F401
     PayloadSizeMismatch, PeerUnavailable, PhaseSchedule, PhaseSkew, PhysParams, RunResult, Scheme, Solver,
     SpanAtLevel, Sweep1dError, TagMismatch, TransportAborted, TransportParams, UnknownInitialCondition,
     apply_config_entry, apply_config_file, cycle_advance, device_count, diamond_schedule, down_triangle_schedule,
-    initial_condition, make_partition, make_spec, max_signal_speed, run, swept_buffer_cells, to_string,
+    initial_condition, make_partition, make_spec, max_signal_speed, measure_fp64_peak, run, swept_buffer_cells, to_string,
     triangle_schedule, version, working_array_extents)

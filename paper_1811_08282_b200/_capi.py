@@ -34,7 +34,9 @@ class s1d_stats(C.Structure):
 
 class s1d_timing(C.Structure):
     _fields_ = [("setup_seconds", C.c_double), ("loop_seconds", C.c_double), ("virtual_seconds", C.c_double),
-                ("h2d_seconds", C.c_double), ("d2h_seconds", C.c_double)]
+                ("h2d_seconds", C.c_double), ("d2h_seconds", C.c_double), ("dominant_seconds", C.c_double),
+                ("dominant_launches", C.c_uint64), ("dominant_point_updates", C.c_uint64),
+                ("dominant_kernel", C.c_char * 32)]
 
 
 _dp = C.POINTER(C.c_double)
@@ -69,6 +71,7 @@ SIGNATURES = {
     "s1d_solve": (C.c_int, [C.c_void_p, _dp, C.c_size_t, _dp, C.c_size_t, C.POINTER(s1d_stats),
                             C.POINTER(s1d_timing)]),
     "s1d_last_error": (C.c_char_p, [C.c_void_p]),
+    "s1d_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)] + _E),
 }
 
 _lib = None

@@ -391,6 +391,10 @@ class EngineTiming:
     virtual_seconds: float = 0.0
     h2d_seconds: float = 0.0
     d2h_seconds: float = 0.0
+    dominant_seconds: float = 0.0
+    dominant_launches: int = 0
+    dominant_point_updates: int = 0
+    dominant_kernel: str = ""
 
 
 @dataclass
@@ -407,7 +411,9 @@ def _stats(s: _capi.s1d_stats, setup: float = 0.0) -> CommStats:
 
 
 def _timing(t: _capi.s1d_timing) -> EngineTiming:
-    return EngineTiming(t.setup_seconds, t.loop_seconds, t.virtual_seconds, t.h2d_seconds, t.d2h_seconds)
+    return EngineTiming(t.setup_seconds, t.loop_seconds, t.virtual_seconds, t.h2d_seconds, t.d2h_seconds,
+                        t.dominant_seconds, t.dominant_launches, t.dominant_point_updates,
+                        t.dominant_kernel.decode())
 
 
 def _dptr(a: np.ndarray):
@@ -494,6 +500,14 @@ class Solver:
             status = lib().s1d_solve(self._h, None, 0, _dptr(out), out.size, C.byref(st), C.byref(tm))
         self._chk(status)
         return out, _stats(st), _timing(tm)
+
+
+def measure_fp64_peak(device: int = 0) -> float:
+    """Sustained FP64 DADD/DMUL instruction rate (ops/s) of one device."""
+    out = C.c_double()
+    e = _errbuf()
+    _check(lib().s1d_measure_fp64_peak(device, C.byref(out), e, 1024), e)
+    return out.value
 
 
 def device_count() -> int:

@@ -44,6 +44,7 @@ struct Shard {
     int dev = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_done = nullptr;
+    cudaEvent_t ev_dom0 = nullptr, ev_dom1 = nullptr; // around the dominant kernel's launches
     std::uint64_t N = 0, nb = 0, start = 0;
     std::uint64_t fstride = 0; // doubles between SoA fields of a state buffer
     double* ic = nullptr;      // resident initial state
@@ -84,6 +85,8 @@ struct Solver {
             if (s.ev_start) cudaEventDestroy(s.ev_start);
             if (s.ev_stop) cudaEventDestroy(s.ev_stop);
             if (s.ev_done) cudaEventDestroy(s.ev_done);
+            if (s.ev_dom0) cudaEventDestroy(s.ev_dom0);
+            if (s.ev_dom1) cudaEventDestroy(s.ev_dom1);
             if (s.st) cudaStreamDestroy(s.st);
         }
         shards.clear();
@@ -103,6 +106,10 @@ struct Solver {
         part = make_partition(cfg);
         m = cycle_advance(cfg.block_width, static_cast<std::uint64_t>(spec.h));
         p = heat_points_per_thread(static_cast<int>(cfg.block_width));
+        if (p < 0)
+            throw Error(S1D_INVALID_WIDTH, "block width " + std::to_string(cfg.block_width) +
+                                               " has no tile decomposition on the B200 path "
+                                               "(needs w/P <= 1024 threads for some P in {2,4,8,16} dividing w)");
 
         int visible = 0;
         if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0)
@@ -143,6 +150,8 @@ struct Solver {
             S1D_CUDA(cudaEventCreate(&s.ev_start));
             S1D_CUDA(cudaEventCreate(&s.ev_stop));
             S1D_CUDA(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
+            S1D_CUDA(cudaEventCreate(&s.ev_dom0));
+            S1D_CUDA(cudaEventCreate(&s.ev_dom1));
             const std::size_t state_bytes = sizeof(double) * s.N * static_cast<std::size_t>(spec.rec);
             S1D_CUDA(cudaMalloc(&s.ic, state_bytes));
             S1D_CUDA(cudaMalloc(&s.state[0], state_bytes));
@@ -217,12 +226,20 @@ struct Solver {
         }
     }
 
+    void record_all(cudaEvent_t Shard::*ev) {
+        for (auto& s : shards) {
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(cudaEventRecord(s.*ev, s.st));
+        }
+    }
+
     void classic_steps(std::int64_t c_begin, std::int64_t c_end, const double** cur_per_shard, int* cur_idx,
-                       s1d_stats& stats) {
+                       s1d_stats& stats, bool dominant = false) {
         // cur_per_shard[g]: buffer holding the current level; results ping-pong
         // through state[0]/state[1] (cur_idx: which one holds the result, -1 = ic).
         for (std::int64_t c = c_begin; c <= c_end; ++c) {
             wait_neighbours();
+            if (dominant && c == c_begin) record_all(&Shard::ev_dom0);
             const int nxt = (*cur_idx == 0) ? 1 : 0;
             for (int g = 0; g < R(); ++g) {
                 Shard& s = shards[static_cast<std::size_t>(g)];
@@ -249,14 +266,16 @@ struct Solver {
                 S1D_CUDA(launch_heat_classic(a, s.st));
                 stats.kernel_launches += 1;
             }
+            if (dominant && c == c_end) record_all(&Shard::ev_dom1);
             record_round();
             *cur_idx = nxt;
             for (int g = 0; g < R(); ++g) cur_per_shard[g] = shards[static_cast<std::size_t>(g)].state[nxt];
         }
     }
 
-    void swept_phase(int kind, std::int64_t j, s1d_stats& stats) {
+    void swept_phase(int kind, std::int64_t j, s1d_stats& stats, bool dom_first = false, bool dom_last = false) {
         wait_neighbours();
+        if (dom_first) record_all(&Shard::ev_dom0);
         const int w = static_cast<int>(cfg.block_width);
         const int src = static_cast<int>((j + 1) & 1), dst = static_cast<int>(j & 1);
         for (int g = 0; g < R(); ++g) {
@@ -294,6 +313,7 @@ struct Solver {
             if (R() > 1 && kind != kUp)
                 stats.edge_bytes_device += sizeof(double) * static_cast<std::uint64_t>(w) * spec.rec;
         }
+        if (dom_last) record_all(&Shard::ev_dom1);
         record_round();
     }
 
@@ -314,20 +334,29 @@ struct Solver {
         std::vector<const double*> cur(static_cast<std::size_t>(R()));
         int cur_idx = -1;
         for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].ic;
+        // Dominant kernel: the Diamond phases when there are any, else the
+        // classic substeps, else the Up/Down pair.
+        const bool dom_diamond = cycles >= 2;
+        const bool dom_classic = !dom_diamond && pad > 0;
+        const bool dom_updown = !dom_diamond && !dom_classic && cycles == 1;
         if (cycles >= 1) {
-            swept_phase(kUp, 0, stats);
-            for (std::int64_t j = 1; j <= cycles; ++j) swept_phase(j == cycles ? kDown : kDiamond, j, stats);
+            swept_phase(kUp, 0, stats, dom_updown, false);
+            for (std::int64_t j = 1; j <= cycles; ++j)
+                swept_phase(j == cycles ? kDown : kDiamond, j, stats, dom_diamond && j == 1,
+                            (dom_diamond && j == cycles - 1) || (dom_updown && j == cycles));
             cur_idx = 0;
             for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].state[0];
         }
-        if (pad > 0) classic_steps(cycles * static_cast<std::int64_t>(m) + 1, total, cur.data(), &cur_idx, stats);
+        if (pad > 0)
+            classic_steps(cycles * static_cast<std::int64_t>(m) + 1, total, cur.data(), &cur_idx, stats, dom_classic);
 
         for (auto& s : shards) {
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaEventRecord(s.ev_stop, s.st));
         }
         sync_all();
-        float worst_ms = 0.0f;
+        float worst_ms = 0.0f, dom_ms = 0.0f;
+        const bool have_dom = dom_diamond || dom_classic || dom_updown;
         int flag = 0;
         for (int g = 0; g < R(); ++g) {
             Shard& s = shards[static_cast<std::size_t>(g)];
@@ -335,6 +364,10 @@ struct Solver {
             float ms = 0.0f;
             S1D_CUDA(cudaEventElapsedTime(&ms, s.ev_start, s.ev_stop));
             worst_ms = std::max(worst_ms, ms);
+            if (have_dom) {
+                S1D_CUDA(cudaEventElapsedTime(&ms, s.ev_dom0, s.ev_dom1));
+                dom_ms = std::max(dom_ms, ms);
+            }
             int f = 0;
             S1D_CUDA(cudaMemcpy(&f, s.err, sizeof(int), cudaMemcpyDeviceToHost));
             flag |= f;
@@ -361,6 +394,22 @@ struct Solver {
             timing_out->setup_seconds = setup_seconds;
             timing_out->loop_seconds = worst_ms * 1e-3;
             timing_out->virtual_seconds = 0.0;
+            timing_out->dominant_seconds = dom_ms * 1e-3;
+            const char* name = "";
+            if (dom_diamond) {
+                timing_out->dominant_launches = static_cast<std::uint64_t>(cycles - 1);
+                timing_out->dominant_point_updates = static_cast<std::uint64_t>(cycles - 1) * m * cfg.grid_size;
+                name = "swept_diamond";
+            } else if (dom_classic) {
+                timing_out->dominant_launches = static_cast<std::uint64_t>(pad);
+                timing_out->dominant_point_updates = static_cast<std::uint64_t>(pad) * cfg.grid_size;
+                name = "classic_substep";
+            } else if (dom_updown) {
+                timing_out->dominant_launches = 2;
+                timing_out->dominant_point_updates = m * cfg.grid_size;
+                name = "swept_up_down";
+            }
+            std::snprintf(timing_out->dominant_kernel, sizeof(timing_out->dominant_kernel), "%s", name);
         }
     }
 

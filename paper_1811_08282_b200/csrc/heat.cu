@@ -23,7 +23,7 @@
 //
 // Edges: the left producer's R edges and the right producer's L edges (2
 // values per level each) stream into a small shared-memory ring per tile
-// (cp.async, kLook levels ahead). The insert of level r lands at x = lo-1, lo (left) and hi-1, hi (right); its
+// (cp.async, kRing-2 levels ahead). The insert of level r lands at x = lo-1, lo (left) and hi-1, hi (right); its
 // shared-memory address is affine in x, so the warp that holds those points
 // reloads them with predicated loads (points further out are don't-care:
 // they are outside the dependency cone). Exports L[d], R[d] are written by
@@ -60,11 +60,10 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
 }
 
 // Incoming edges stream through a per-tile ring of kRing levels (2 values per
-// level per side) filled with cp.async kLook levels ahead of use, so shared
+// level per side) filled with cp.async kRing-2 levels ahead of use, so shared
 // memory per tile is O(1) in w. Ring index of (level r, x) is affine in x and
 // wrapped with a mask, so predicated insert loads stay contiguous.
 constexpr int kRing = 32;             // levels held per side (power of two)
-constexpr int kLook = 16;             // cp.async lookahead in levels (< kRing)
 constexpr int kRingMask = 2 * kRing - 1;
 __host__ __device__ inline int tile_edge_stride(int) { return 4 * kRing; }
 
@@ -157,8 +156,8 @@ __device__ __forceinline__ void insert_level(const TileCtx<P>& c, double (&v)[P]
     }
 }
 
-template <int P, int KIND>
-__global__ void __launch_bounds__(256) heat_tile_kernel(const TileArgs a, int G) {
+template <int P, int KIND, int MAXT>
+__global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ double sm[];
     const int w = a.w, m = a.m;
     const int tt = w / P;                 // threads per tile
@@ -201,11 +200,13 @@ __global__ void __launch_bounds__(256) heat_tile_kernel(const TileArgs a, int G)
             for (int k = 0; k < P; ++k) v[k] = src[k];
         }
     }
-    // Edge streaming (Diamond/Down): thread lt == 0 of each live tile copies
-    // level q's 2+2 edge values into ring slot q mod kRing, kLook levels ahead.
+    // Edge streaming (Diamond/Down). The tile's threads load levels
+    // 1..min(m, kRing) cooperatively; for longer tiles thread lt == 0 then
+    // queues level r+kRing-1 into the slot freed by level r-1 (cp.async, one
+    // group per level) and waits so that level r+1 has landed before barrier r.
     const double* pR = nullptr;
     const double* pL = nullptr;
-    const bool feeder = live && c.lt == 0 && KIND != kUp;
+    const bool feeder = live && c.lt == 0 && KIND != kUp && m > kRing;
     if (KIND != kUp) {
         if (live) {
             if (a.seam) {
@@ -215,31 +216,23 @@ __global__ void __launch_bounds__(256) heat_tile_kernel(const TileArgs a, int G)
                 pR = (b > 0) ? a.in_R + (std::size_t)(b - 1) * w : a.peer_R;
                 pL = a.in_L + (std::size_t)b * w;
             }
-        }
-        if (feeder) {
-#pragma unroll 1
-            for (int q = 0; q < kLook; ++q) {
-                if (q < m) {
-                    cp_async16(einR + ((2 * q) & kRingMask), pR + 2 * q);
-                    cp_async16(einL + ((2 * q) & kRingMask), pL + 2 * q);
-                }
-                cp_async_commit();
+            const int n0 = 2 * (m < kRing ? m : kRing);
+            for (int i = c.lt; i < n0; i += tt) {
+                einR[i] = pR[i];
+                einL[i] = pL[i];
             }
-            cp_async_wait<kLook - 1>(); // level 1 landed
         }
         __syncthreads();
     }
-    // Called before the barrier of level r: queue level r+kLook, and make sure
-    // level r+1 has landed (visible to all after the barrier).
     auto feed = [&](int r) {
         if (feeder) {
-            const int q = r + kLook - 1; // 0-based level index of level r+kLook
+            const int q = r + kRing - 2; // 0-based index of level r+kRing-1
             if (q < m) {
                 cp_async16(einR + ((2 * q) & kRingMask), pR + 2 * q);
                 cp_async16(einL + ((2 * q) & kRingMask), pL + 2 * q);
             }
             cp_async_commit();
-            cp_async_wait<kLook - 1>();
+            cp_async_wait<kRing - 2>();
         }
     };
 
@@ -292,19 +285,20 @@ __global__ void __launch_bounds__(256) heat_tile_kernel(const TileArgs a, int G)
 int tiles_per_cta(int w, int p) {
     const int tt = w / p;
     int G = 1;
+    if (tt > 256) return 1;
     while ((G * 2) * tt <= 256 && G * 2 <= 64) G *= 2;
     return G;
 }
 
-template <int P>
+template <int P, int MAXT = 256>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     const int tt = a.w / P;
     const int G = tiles_per_cta(a.w, P);
     const int nt = G * tt;
     const size_t smem = sizeof(double) * (4 * (size_t)G * (tt + 2) + (size_t)G * tile_edge_stride(a.w));
-    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P, kUp>
-                                     : kind == kDiamond ? heat_tile_kernel<P, kDiamond>
-                                                        : heat_tile_kernel<P, kDown>;
+    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P, kUp, MAXT>
+                                     : kind == kDiamond ? heat_tile_kernel<P, kDiamond, MAXT>
+                                                        : heat_tile_kernel<P, kDown, MAXT>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -321,13 +315,13 @@ int heat_points_per_thread(int w) {
         const int p = std::atoi(e);
         if ((p == 1 || p == 2 || p == 4 || p == 8 || p == 16) && w % p == 0 && w / p <= 256) return p;
     }
-    // Largest P in {2,4,8,16} dividing w that keeps >= 128 threads per tile,
-    // at least 2, and never more than 256 threads per tile.
+    // 256 threads per tile for wide tiles (P = w/256); P = 4 for narrow ones
+    // (several tiles per CTA); always P | w, 2 <= P <= 16, w/P <= 256.
     int p = 2;
-    for (int c : {4, 8, 16})
-        if (w % c == 0 && w / c >= 128) p = c;
+    if (w % 4 == 0) p = 4;
     while (w / p > 256 && w % (2 * p) == 0 && p < 16) p *= 2;
-    return p;
+    if (w / p > 1024) return -1; // no valid decomposition (caller reports it)
+    return p;                    // w/p in (256, 1024] only for w = 2 mod 4 (P = 2, wide CTA)
 }
 
 cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st) {
@@ -344,7 +338,8 @@ cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st) {
-    if (a.w / a.p > 256 || a.w % a.p) return cudaErrorInvalidValue;
+    if (a.w % a.p || a.w / a.p > 1024) return cudaErrorInvalidValue;
+    if (a.w / a.p > 256) return a.p == 2 ? launch_tile_p<2, 1024>(kind, a, st) : cudaErrorInvalidValue;
     switch (a.p) {
     case 1: return launch_tile_p<1>(kind, a, st);
     case 2: return launch_tile_p<2>(kind, a, st);

@@ -48,7 +48,7 @@ def test_decomp_cases(gpu, n, w, ranks, wf, steps, scheme):
         assert_bitwise(got, want)
 
 
-@pytest.mark.parametrize("w", [4, 6, 8, 12, 16, 32, 64, 128, 256, 512, 1024, 2048, 4096])
+@pytest.mark.parametrize("w", [4, 6, 8, 12, 16, 32, 64, 128, 256, 512, 514, 1000, 1024, 2048, 4096])
 def test_width_sweep_unaligned(gpu, w):
     n = max(4 * w, 1 << 13)
     n -= n % w
