@@ -52,6 +52,7 @@ struct Shard {
     double* EL[2] = {nullptr, nullptr};
     double* ER[2] = {nullptr, nullptr};
     int* err = nullptr;
+    double* staging = nullptr; // AoS (vpp = 3) upload/download buffer (Euler)
     const double* final_state = nullptr;
 };
 
@@ -65,6 +66,7 @@ struct Solver {
     int ndev = 1;
     std::uint64_t m = 0;
     int p = 2;
+    bool euler = false, flat = false;
     double setup_seconds = 0.0;
     std::string last_error;
     std::vector<double> host_ic;
@@ -82,6 +84,7 @@ struct Solver {
                 cudaFree(s.ER[k]);
             }
             cudaFree(s.err);
+            cudaFree(s.staging);
             if (s.ev_start) cudaEventDestroy(s.ev_start);
             if (s.ev_stop) cudaEventDestroy(s.ev_stop);
             if (s.ev_done) cudaEventDestroy(s.ev_done);
@@ -101,15 +104,23 @@ struct Solver {
         cfg = in;
         finalize(cfg, true);
         spec = make_spec(cfg.equation, cfg.method);
-        if (cfg.equation != S1D_HEAT)
-            throw Error(S1D_INVALID_CONFIG, "equation not yet supported by the B200 path");
+        euler = cfg.equation == S1D_EULER;
+        flat = euler && cfg.method == S1D_FLATTENING;
         part = make_partition(cfg);
         m = cycle_advance(cfg.block_width, static_cast<std::uint64_t>(spec.h));
-        p = heat_points_per_thread(static_cast<int>(cfg.block_width));
-        if (p < 0)
-            throw Error(S1D_INVALID_WIDTH, "block width " + std::to_string(cfg.block_width) +
-                                               " has no tile decomposition on the B200 path "
-                                               "(needs w/P <= 1024 threads for some P in {2,4,8,16} dividing w)");
+        if (cfg.scheme == S1D_SWEPT) {
+            if (!euler) {
+                p = heat_points_per_thread(static_cast<int>(cfg.block_width));
+                if (p < 0)
+                    throw Error(S1D_INVALID_WIDTH,
+                                "block width " + std::to_string(cfg.block_width) +
+                                    " has no tile decomposition on the B200 path "
+                                    "(needs w/P <= 1024 threads for some P in {2,4,8,16} dividing w)");
+            } else if (euler_tile_smem_bytes(flat ? 1 : 0, static_cast<int>(cfg.block_width)) > 227 * 1024) {
+                throw Error(S1D_INVALID_WIDTH, "block width " + std::to_string(cfg.block_width) +
+                                                   " exceeds the shared-memory-resident Euler tile (227 KB per CTA)");
+            }
+        }
 
         int visible = 0;
         if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0)
@@ -158,6 +169,7 @@ struct Solver {
             S1D_CUDA(cudaMalloc(&s.state[1], state_bytes));
             S1D_CUDA(cudaMalloc(&s.err, sizeof(int)));
             S1D_CUDA(cudaMemset(s.err, 0, sizeof(int)));
+            if (euler) S1D_CUDA(cudaMalloc(&s.staging, sizeof(double) * 3 * s.N));
             if (cfg.scheme == S1D_SWEPT) {
                 const std::size_t edge_bytes = sizeof(double) * s.nb * w * static_cast<std::size_t>(spec.rec);
                 for (int k = 0; k < 2; ++k) {
@@ -178,28 +190,33 @@ struct Solver {
         }
     }
 
-    // Global-order host state (vpp doubles per point) -> per-shard SoA ic.
+    // Global-order host state (vpp doubles per point) -> per-shard SoA ic
+    // (Euler: make_cell, Q0 = Q1 = v, Pr = 0; inc/kernels.hpp:144-149).
     void upload(const double* host) {
-        const int vpp = spec.vpp;
         for (auto& s : shards) {
             S1D_CUDA(cudaSetDevice(s.dev));
-            if (vpp == 1) {
+            if (!euler) {
                 S1D_CUDA(cudaMemcpyAsync(s.ic, host + s.start, sizeof(double) * s.N, cudaMemcpyHostToDevice, s.st));
             } else {
-                throw Error(S1D_INTERNAL, "multi-value upload not implemented");
+                S1D_CUDA(cudaMemcpyAsync(s.staging, host + 3 * s.start, sizeof(double) * 3 * s.N,
+                                         cudaMemcpyHostToDevice, s.st));
+                S1D_CUDA(launch_euler_unpack(s.staging, s.ic, s.N, s.fstride, spec.rec, s.st));
             }
         }
     }
 
+    // Final state -> global-order host array (extract: Q0 for Euler,
+    // inc/kernels.hpp:150-154; the current level for heat).
     void download(double* host) {
-        const int vpp = spec.vpp;
         for (auto& s : shards) {
             S1D_CUDA(cudaSetDevice(s.dev));
-            if (vpp == 1) {
+            if (!euler) {
                 S1D_CUDA(cudaMemcpyAsync(host + s.start, s.final_state, sizeof(double) * s.N,
                                          cudaMemcpyDeviceToHost, s.st));
             } else {
-                throw Error(S1D_INTERNAL, "multi-value download not implemented");
+                S1D_CUDA(launch_euler_pack(s.final_state, s.staging, s.N, s.fstride, s.st));
+                S1D_CUDA(cudaMemcpyAsync(host + 3 * s.start, s.staging, sizeof(double) * 3 * s.N,
+                                         cudaMemcpyDeviceToHost, s.st));
             }
         }
         sync_all();
@@ -240,7 +257,7 @@ struct Solver {
         for (std::int64_t c = c_begin; c <= c_end; ++c) {
             wait_neighbours();
             if (dominant && c == c_begin) record_all(&Shard::ev_dom0);
-            const int nxt = (*cur_idx == 0) ? 1 : 0;
+            const int nxt = euler ? 0 : ((*cur_idx == 0) ? 1 : 0);
             for (int g = 0; g < R(); ++g) {
                 Shard& s = shards[static_cast<std::size_t>(g)];
                 Shard& L = left_of(g);
@@ -263,7 +280,13 @@ struct Solver {
                 a.dt_dx = cfg.dt_dx;
                 a.error_flag = s.err;
                 S1D_CUDA(cudaSetDevice(s.dev));
-                S1D_CUDA(launch_heat_classic(a, s.st));
+                if (euler) {
+                    // in place on state[0] (cur == state[0] for every shard)
+                    a.out = s.state[0];
+                    S1D_CUDA(launch_euler_classic(flat ? 1 : 0, a, s.st));
+                } else {
+                    S1D_CUDA(launch_heat_classic(a, s.st));
+                }
                 stats.kernel_launches += 1;
             }
             if (dominant && c == c_end) record_all(&Shard::ev_dom1);
@@ -308,7 +331,8 @@ struct Solver {
             a.dt_dx = cfg.dt_dx;
             a.error_flag = s.err;
             S1D_CUDA(cudaSetDevice(s.dev));
-            S1D_CUDA(launch_heat_tile(kind, a, s.st));
+            if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, a, s.st));
+            else S1D_CUDA(launch_heat_tile(kind, a, s.st));
             stats.kernel_launches += 1;
             if (R() > 1 && kind != kUp)
                 stats.edge_bytes_device += sizeof(double) * static_cast<std::uint64_t>(w) * spec.rec;
@@ -327,6 +351,12 @@ struct Solver {
         for (auto& s : shards) {
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaMemsetAsync(s.err, 0, sizeof(int), s.st));
+            // Euler classic substeps run in place on state[0]; seed it with the
+            // initial records when no swept phase writes it first (placement
+            // of the IC is setup in the reference, outside the timed loop).
+            if (euler && cycles == 0 && pad > 0)
+                S1D_CUDA(cudaMemcpyAsync(s.state[0], s.ic, sizeof(double) * s.N * spec.rec, cudaMemcpyDeviceToDevice,
+                                         s.st));
             S1D_CUDA(cudaEventRecord(s.ev_start, s.st));
         }
         record_round();
@@ -347,8 +377,14 @@ struct Solver {
             cur_idx = 0;
             for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].state[0];
         }
-        if (pad > 0)
+        if (pad > 0) {
+            if (euler && cycles == 0) {
+                cur_idx = 0;
+                for (int g = 0; g < R(); ++g)
+                    cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].state[0];
+            }
             classic_steps(cycles * static_cast<std::int64_t>(m) + 1, total, cur.data(), &cur_idx, stats, dom_classic);
+        }
 
         for (auto& s : shards) {
             S1D_CUDA(cudaSetDevice(s.dev));

@@ -1,0 +1,439 @@
+// Euler (Sod) kernels for sm_100a, FP64: second-order MUSCL/minmod
+// predictor-corrector with a Rusanov flux and Roe-averaged signal speed.
+//
+// Two data-structure strategies of the reference (inc/kernels.hpp:128-185):
+//   lengthening (EulerLenModel, S=4, h=1, record Q0,Q1,Pr = 7 doubles):
+//     c%4==1 Pr <- ratio(p(Q0));  c%4==2 Q1 <- Q0 - dt/2dx (F+ - F-)[Q0,Pr]
+//     c%4==3 Pr <- ratio(p(Q1));  c%4==0 Q0 <- Q0 - dt/dx  (F+ - F-)[Q1,Pr]
+//   flattening (EulerFlatModel, S=2, h=2, record Q0,Q1 = 6 doubles): the
+//     ratios are recomputed inline from a 5-point pressure window.
+//
+// State in HBM is SoA by field: field f of point i at st[f*fstride + i]
+// (f: 0..2 Q0, 3..5 Q1, 6 Pr).
+//
+// Every interface flux and every pressure is computed ONCE and shared by the
+// cells that read it (the reference evaluates each flux twice and each
+// pressure 3-5 times); the arguments are identical, so results are too.
+//
+//   euler_len_classic<K>, euler_flat_classic<F>: one substep per launch
+//     (reference classic_worker, engines_impl.hpp:201-213), in place.
+//   euler_tile<FLAT,KIND>: one swept phase (Up / Diamond / Down), the tile's
+//     records resident in shared memory; each phase maps the CTA's threads
+//     onto exactly the points of the level's span (no wasted or speculative
+//     arithmetic, so the non-physical-state flag is exact).
+#include <cstdint>
+
+#include "euler_math.cuh"
+#include "kernels.hpp"
+
+namespace s1d {
+namespace {
+
+constexpr int kClassicB = 256; // points per CTA in the classic kernels
+
+struct Fields {
+    double* st;
+    std::uint64_t N, fs;
+    const double* hl;
+    std::uint64_t hlfs;
+    const double* hr;
+    std::uint64_t hrfs;
+    int h;
+    __device__ __forceinline__ double ld(int f, std::int64_t x) const {
+        if (x < 0) return hl[(std::uint64_t)(x + h) + f * hlfs];
+        if ((std::uint64_t)x >= N) return hr[((std::uint64_t)x - N) + f * hrfs];
+        return st[(std::uint64_t)x + f * fs];
+    }
+};
+
+__device__ __forceinline__ Fields fields_of(const ClassicArgs& a) {
+    return Fields{a.out, a.N, a.fstride, a.halo_l, a.halo_l_fstride, a.halo_r, a.halo_r_fstride, a.h};
+}
+
+__device__ __forceinline__ void raise_flag(int* flag, bool bad) {
+    if (__any_sync(__activemask(), bad) && bad) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// classic, lengthening. KIND = counter % 4 (1 PR on Q0, 2 predictor, 3 PR on
+// Q1, 0 corrector).
+// ---------------------------------------------------------------------------
+template <int KIND>
+__global__ void __launch_bounds__(kClassicB) euler_len_classic(const ClassicArgs a) {
+    __shared__ double sh[3][kClassicB + 2];
+    const Fields F = fields_of(a);
+    const double gamma = a.gamma;
+    bool bad = false;
+    for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * kClassicB; i0 < a.N; i0 += (std::uint64_t)gridDim.x * kClassicB) {
+        const int nb = (int)min((std::uint64_t)kClassicB, a.N - i0);
+        if (KIND & 1) {
+            const int s = (KIND == 1) ? 0 : 3;
+            for (int t = threadIdx.x; t < nb + 2; t += blockDim.x) {
+                const std::int64_t x = (std::int64_t)i0 + t - 1;
+                sh[0][t] = em::pressure(F.ld(s, x), F.ld(s + 1, x), F.ld(s + 2, x), gamma, bad);
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < nb; t += blockDim.x)
+                a.out[i0 + t + 6 * a.fstride] = em::ratio(sh[0][t], sh[0][t + 1], sh[0][t + 2]);
+        } else {
+            const bool fin = (KIND == 0);
+            const int rs = fin ? 3 : 0, ws = fin ? 0 : 3;
+            const double factor = fin ? a.dt_dx : em::mul(0.5, a.dt_dx);
+            // interface t sits between points i0+t-1 and i0+t
+            for (int t = threadIdx.x; t < nb + 1; t += blockDim.x) {
+                const std::int64_t x = (std::int64_t)i0 + t;
+                double f0, f1, f2;
+                em::iflux(F.ld(rs, x - 1), F.ld(rs + 1, x - 1), F.ld(rs + 2, x - 1), F.ld(rs, x), F.ld(rs + 1, x),
+                          F.ld(rs + 2, x), F.ld(6, x - 1), F.ld(6, x), gamma, f0, f1, f2, bad);
+                sh[0][t] = f0;
+                sh[1][t] = f1;
+                sh[2][t] = f2;
+            }
+            __syncthreads();
+            for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+                const std::uint64_t x = i0 + t;
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    a.out[x + (ws + k) * a.fstride] =
+                        em::update(a.out[x + k * a.fstride], factor, sh[k][t + 1], sh[k][t]);
+            }
+        }
+        __syncthreads();
+    }
+    raise_flag(a.error_flag, bad);
+}
+
+// classic, flattening. FIN = 0 predictor (Q1 <- from Q0), 1 corrector.
+template <int FIN>
+__global__ void __launch_bounds__(kClassicB) euler_flat_classic(const ClassicArgs a) {
+    __shared__ double sp[kClassicB + 4];
+    __shared__ double sf[3][kClassicB + 1];
+    const Fields F = fields_of(a);
+    const double gamma = a.gamma;
+    const int s = FIN ? 3 : 0, ws = FIN ? 0 : 3;
+    const double factor = FIN ? a.dt_dx : em::mul(0.5, a.dt_dx);
+    bool bad = false;
+    for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * kClassicB; i0 < a.N; i0 += (std::uint64_t)gridDim.x * kClassicB) {
+        const int nb = (int)min((std::uint64_t)kClassicB, a.N - i0);
+        for (int t = threadIdx.x; t < nb + 4; t += blockDim.x) { // sp[t] = p(i0 + t - 2)
+            const std::int64_t x = (std::int64_t)i0 + t - 2;
+            sp[t] = em::pressure(F.ld(s, x), F.ld(s + 1, x), F.ld(s + 2, x), gamma, bad);
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nb + 1; t += blockDim.x) { // interface between i0+t-1 and i0+t
+            const std::int64_t x = (std::int64_t)i0 + t;
+            const double rl = em::ratio(sp[t], sp[t + 1], sp[t + 2]);     // ratio at x-1
+            const double rr = em::ratio(sp[t + 1], sp[t + 2], sp[t + 3]); // ratio at x
+            double f0, f1, f2;
+            em::iflux(F.ld(s, x - 1), F.ld(s + 1, x - 1), F.ld(s + 2, x - 1), F.ld(s, x), F.ld(s + 1, x),
+                      F.ld(s + 2, x), rl, rr, gamma, f0, f1, f2, bad);
+            sf[0][t] = f0;
+            sf[1][t] = f1;
+            sf[2][t] = f2;
+        }
+        __syncthreads();
+        for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+            const std::uint64_t x = i0 + t;
+#pragma unroll
+            for (int k = 0; k < 3; ++k)
+                a.out[x + (ws + k) * a.fstride] = em::update(a.out[x + k * a.fstride], factor, sf[k][t + 1], sf[k][t]);
+        }
+        __syncthreads();
+    }
+    raise_flag(a.error_flag, bad);
+}
+
+// ---------------------------------------------------------------------------
+// swept tile (one CTA per tile)
+// ---------------------------------------------------------------------------
+constexpr int kERing = 16; // ring levels per side
+constexpr int kELook = 8;  // cp.async lookahead (levels)
+
+__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
+
+template <int FLAT>
+struct TileGeom {
+    static constexpr int H = FLAT ? 2 : 1;
+    static constexpr int REC = FLAT ? 6 : 7;
+    static constexpr int LVL = 2 * H * REC;   // doubles per level per side in an edge
+    static constexpr int CHUNKS = LVL / 2;    // 16-byte chunks per level per side
+};
+
+inline std::size_t euler_tile_smem(int flat, int w) {
+    const int H = flat ? 2 : 1, REC = flat ? 6 : 7;
+    const std::size_t W2 = (std::size_t)w + 2 * H;
+    const std::size_t s = REC * W2 + (W2 + 1) + 3 * (W2 + 1) + 2 * (std::size_t)kERing * 2 * H * REC;
+    return s * sizeof(double);
+}
+
+template <int FLAT, int KIND>
+__global__ void __launch_bounds__(256) euler_tile(const TileArgs a) {
+    using G = TileGeom<FLAT>;
+    constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
+    extern __shared__ double sm[];
+    const int w = a.w, m = a.m, b = blockIdx.x, t = threadIdx.x, NT = blockDim.x;
+    const int W2 = w + 2 * H;
+    double* S = sm;                      // [REC][W2] records, local x in [0, W2)
+    double* P = S + REC * W2;            // [W2+1] pressures
+    double* Fx = P + (W2 + 1);           // [3][W2+1] interface fluxes (interface x: between x-1 and x)
+    double* ring = Fx + 3 * (W2 + 1);    // [2 sides][kERing][LVL]
+    const double gamma = a.gamma;
+    const double dt_dx = a.dt_dx;
+    bool bad = false;
+
+    const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
+    const std::int64_t g0 = centre - w / 2 - H; // shard position of local x = 0
+
+    // producers' edges (Diamond/Down)
+    const double* pR = nullptr;
+    const double* pL = nullptr;
+    const std::size_t tstride = (std::size_t)w * REC; // edge doubles per tile per side
+    // feeders: threads [0, CHUNKS) copy the left (R-edge) chunks, [CHUNKS, 2*CHUNKS) the right
+    const bool feeder = KIND != kUp && t < 2 * G::CHUNKS;
+    const int fside = t < G::CHUNKS ? 0 : 1, fchunk = t % G::CHUNKS;
+    auto issue = [&](int q) { // level q (1-based) into its ring slot
+        if (feeder && q <= m) {
+            const double* src = (fside == 0 ? pR : pL) + (std::size_t)(q - 1) * LVL + 2 * fchunk;
+            double* dst = ring + ((std::size_t)fside * kERing + (q - 1) % kERing) * LVL + 2 * fchunk;
+            cp_async16(dst, src);
+        }
+    };
+    // copy level q's ring slot into S: left records at x in [lo-H, lo+H),
+    // right at [hi-H, hi+H) with lo/hi the span of level q.
+    auto insert = [&](int q) {
+        const int lo = w / 2 + H - q * H, hi = w / 2 + H + q * H;
+        for (int i = t; i < 2 * LVL; i += NT) {
+            const int side = i / LVL, j = i % LVL, rec = j / REC, f = j % REC;
+            const int x = side == 0 ? lo - H + rec : hi - H + rec;
+            S[f * W2 + x] = ring[((std::size_t)side * kERing + (q - 1) % kERing) * LVL + j];
+        }
+    };
+
+    if (KIND == kUp) {
+        for (int f = 0; f < REC; ++f)
+            for (int x = H + t; x < w + H; x += NT)
+                S[f * W2 + x] = a.state_in[(std::size_t)f * a.fstride + (std::size_t)(g0 + x)];
+    } else {
+        if (a.seam) {
+            pR = a.in_R + (std::size_t)b * tstride;
+            pL = (b + 1 < a.nb) ? a.in_L + (std::size_t)(b + 1) * tstride : a.peer_L;
+        } else {
+            pR = (b > 0) ? a.in_R + (std::size_t)(b - 1) * tstride : a.peer_R;
+            pL = a.in_L + (std::size_t)b * tstride;
+        }
+        for (int q = 1; q <= kELook; ++q) {
+            issue(q);
+            if (feeder) cp_async_commit();
+        }
+        if (feeder) cp_async_wait<kELook - 1>();
+        __syncthreads();
+        insert(1);
+    }
+    __syncthreads();
+
+    // One level: counter c, span [lo, hi). `between` runs after the level's
+    // last reads of S outside the span and before its final barrier (inserts
+    // of the next level, ring refill).
+    auto level = [&](std::int64_t c, int lo, int hi, auto&& between) {
+        if (!FLAT) {
+            if (c & 1) {
+                const int s = ((c & 3) == 1) ? 0 : 3;
+                for (int x = lo - 1 + t; x < hi + 1; x += NT)
+                    P[x] = em::pressure(S[s * W2 + x], S[(s + 1) * W2 + x], S[(s + 2) * W2 + x], gamma, bad);
+                between(0);
+                __syncthreads();
+                for (int x = lo + t; x < hi; x += NT) S[6 * W2 + x] = em::ratio(P[x - 1], P[x], P[x + 1]);
+                between(1);
+            } else {
+                const bool fin = (c & 3) == 0;
+                const int rs = fin ? 3 : 0, ws = fin ? 0 : 3;
+                const double factor = fin ? dt_dx : em::mul(0.5, dt_dx);
+                for (int x = lo + t; x < hi + 1; x += NT) {
+                    double f0, f1, f2;
+                    em::iflux(S[rs * W2 + x - 1], S[(rs + 1) * W2 + x - 1], S[(rs + 2) * W2 + x - 1], S[rs * W2 + x],
+                              S[(rs + 1) * W2 + x], S[(rs + 2) * W2 + x], S[6 * W2 + x - 1], S[6 * W2 + x], gamma, f0,
+                              f1, f2, bad);
+                    Fx[x] = f0;
+                    Fx[(W2 + 1) + x] = f1;
+                    Fx[2 * (W2 + 1) + x] = f2;
+                }
+                between(0);
+                __syncthreads();
+                for (int x = lo + t; x < hi; x += NT) {
+#pragma unroll
+                    for (int k = 0; k < 3; ++k)
+                        S[(ws + k) * W2 + x] =
+                            em::update(S[k * W2 + x], factor, Fx[k * (W2 + 1) + x + 1], Fx[k * (W2 + 1) + x]);
+                }
+                between(1);
+            }
+        } else {
+            const bool fin = (c & 1) == 0;
+            const int s = fin ? 3 : 0, ws = fin ? 0 : 3;
+            const double factor = fin ? dt_dx : em::mul(0.5, dt_dx);
+            for (int x = lo - 2 + t; x < hi + 2; x += NT)
+                P[x] = em::pressure(S[s * W2 + x], S[(s + 1) * W2 + x], S[(s + 2) * W2 + x], gamma, bad);
+            __syncthreads();
+            for (int x = lo + t; x < hi + 1; x += NT) {
+                const double rl = em::ratio(P[x - 2], P[x - 1], P[x]);
+                const double rr = em::ratio(P[x - 1], P[x], P[x + 1]);
+                double f0, f1, f2;
+                em::iflux(S[s * W2 + x - 1], S[(s + 1) * W2 + x - 1], S[(s + 2) * W2 + x - 1], S[s * W2 + x],
+                          S[(s + 1) * W2 + x], S[(s + 2) * W2 + x], rl, rr, gamma, f0, f1, f2, bad);
+                Fx[x] = f0;
+                Fx[(W2 + 1) + x] = f1;
+                Fx[2 * (W2 + 1) + x] = f2;
+            }
+            between(0);
+            __syncthreads();
+            for (int x = lo + t; x < hi; x += NT) {
+#pragma unroll
+                for (int k = 0; k < 3; ++k)
+                    S[(ws + k) * W2 + x] =
+                        em::update(S[k * W2 + x], factor, Fx[k * (W2 + 1) + x + 1], Fx[k * (W2 + 1) + x]);
+            }
+            between(1);
+        }
+        __syncthreads();
+    };
+
+    auto export_level = [&](int d, int lo, int hi) {
+        double* oL = a.out_L + (std::size_t)b * tstride + (std::size_t)d * LVL;
+        double* oR = a.out_R + (std::size_t)b * tstride + (std::size_t)d * LVL;
+        for (int i = t; i < 2 * LVL; i += NT) {
+            const int side = i / LVL, j = i % LVL, rec = j / REC, f = j % REC;
+            const int x = side == 0 ? lo + rec : hi - 2 * H + rec;
+            (side == 0 ? oL : oR)[j] = S[f * W2 + x];
+        }
+    };
+
+    const std::int64_t base = a.base;
+    if (KIND != kUp) {
+        for (int r = 1; r <= m; ++r) {
+            const int lo = w / 2 + H - r * H, hi = w / 2 + H + r * H;
+            if (feeder) { // queue level r+kELook; level r+1 must land before the phase barrier
+                issue(r + kELook);
+                cp_async_commit();
+            }
+            level(base + r, lo, hi, [&](int phase) {
+                if (phase == 0) {
+                    if (feeder) cp_async_wait<kELook - 1>();
+                } else if (r < m) {
+                    insert(r + 1);
+                }
+            });
+        }
+    }
+    if (KIND != kDown) {
+        export_level(0, H, w + H);
+        for (int r = m + 1; r <= 2 * m - 1; ++r) {
+            const int d = r - m, lo = H + d * H, hi = w + H - d * H;
+            level(base + r, lo, hi, [](int) {});
+            export_level(d, lo, hi);
+        }
+    } else {
+        for (int f = 0; f < REC; ++f)
+            for (int x = H + t; x < w + H; x += NT) {
+                const std::uint64_t gp = (std::uint64_t)(g0 + x);
+                if (gp < a.N) a.state_out[(std::size_t)f * a.fstride + gp] = S[f * W2 + x];
+                else a.state_right[(std::size_t)f * a.right_fstride + (gp - a.N)] = S[f * W2 + x];
+            }
+    }
+    raise_flag(a.error_flag, bad);
+}
+
+template <int FLAT>
+cudaError_t launch_tile_f(int kind, const TileArgs& a, cudaStream_t st) {
+    const size_t smem = euler_tile_smem(FLAT, a.w);
+    void (*k)(const TileArgs) = kind == kUp ? euler_tile<FLAT, kUp>
+                                : kind == kDiamond ? euler_tile<FLAT, kDiamond>
+                                                   : euler_tile<FLAT, kDown>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    int nt = ((a.w + 2 * TileGeom<FLAT>::H + 31) / 32) * 32;
+    if (nt > 256) nt = 256;
+    if (nt < 2 * TileGeom<FLAT>::CHUNKS) nt = 32 * ((2 * TileGeom<FLAT>::CHUNKS + 31) / 32);
+    k<<<a.nb, nt, smem, st>>>(a);
+    return cudaGetLastError();
+}
+
+__global__ void unpack_kernel(const double* __restrict__ aos, double* __restrict__ st, std::uint64_t N,
+                              std::uint64_t fs, int rec) {
+    for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < N;
+         i += (std::uint64_t)gridDim.x * blockDim.x) {
+        const double q0 = aos[3 * i], q1 = aos[3 * i + 1], q2 = aos[3 * i + 2];
+        st[i] = q0;
+        st[i + fs] = q1;
+        st[i + 2 * fs] = q2;
+        st[i + 3 * fs] = q0;
+        st[i + 4 * fs] = q1;
+        st[i + 5 * fs] = q2;
+        if (rec == 7) st[i + 6 * fs] = 0.0; // make_cell: Pr = 0 (inc/kernels.hpp:144-149)
+    }
+}
+
+__global__ void pack_kernel(const double* __restrict__ st, double* __restrict__ aos, std::uint64_t N,
+                            std::uint64_t fs) {
+    for (std::uint64_t i = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; i < N;
+         i += (std::uint64_t)gridDim.x * blockDim.x) {
+        aos[3 * i] = st[i];
+        aos[3 * i + 1] = st[i + fs];
+        aos[3 * i + 2] = st[i + 2 * fs];
+    }
+}
+
+unsigned grid_for(std::uint64_t n, int per_block) {
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    std::uint64_t blocks = (n + per_block - 1) / per_block;
+    const std::uint64_t cap = (std::uint64_t)sms * 16;
+    if (blocks > cap) blocks = cap;
+    return (unsigned)(blocks ? blocks : 1);
+}
+
+} // namespace
+
+cudaError_t launch_euler_classic(int flat, const ClassicArgs& a, cudaStream_t st) {
+    const unsigned grid = grid_for(a.N, kClassicB);
+    if (flat) {
+        if (a.counter & 1) euler_flat_classic<0><<<grid, kClassicB, 0, st>>>(a);
+        else euler_flat_classic<1><<<grid, kClassicB, 0, st>>>(a);
+    } else {
+        switch (a.counter & 3) {
+        case 1: euler_len_classic<1><<<grid, kClassicB, 0, st>>>(a); break;
+        case 2: euler_len_classic<2><<<grid, kClassicB, 0, st>>>(a); break;
+        case 3: euler_len_classic<3><<<grid, kClassicB, 0, st>>>(a); break;
+        default: euler_len_classic<0><<<grid, kClassicB, 0, st>>>(a); break;
+        }
+    }
+    return cudaGetLastError();
+}
+
+cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_t st) {
+    return flat ? launch_tile_f<1>(kind, a, st) : launch_tile_f<0>(kind, a, st);
+}
+
+cudaError_t launch_euler_unpack(const double* aos, double* st_fields, std::uint64_t N, std::uint64_t fs, int rec,
+                                cudaStream_t st) {
+    unpack_kernel<<<grid_for(N, 256), 256, 0, st>>>(aos, st_fields, N, fs, rec);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_euler_pack(const double* st_fields, double* aos, std::uint64_t N, std::uint64_t fs,
+                              cudaStream_t st) {
+    pack_kernel<<<grid_for(N, 256), 256, 0, st>>>(st_fields, aos, N, fs);
+    return cudaGetLastError();
+}
+
+std::size_t euler_tile_smem_bytes(int flat, int w) { return euler_tile_smem(flat, w); }
+
+} // namespace s1d

@@ -59,4 +59,14 @@ cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st);
 cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st);
 int heat_points_per_thread(int w);
 
+// Euler (flat = 0 lengthening, 1 flattening). Classic kernels update `out`
+// in place (fields written by a substep are never read by it).
+cudaError_t launch_euler_classic(int flat, const ClassicArgs& a, cudaStream_t st);
+cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_t st);
+cudaError_t launch_euler_unpack(const double* aos, double* st_fields, std::uint64_t N, std::uint64_t fs, int rec,
+                                cudaStream_t st);
+cudaError_t launch_euler_pack(const double* st_fields, double* aos, std::uint64_t N, std::uint64_t fs,
+                              cudaStream_t st);
+std::size_t euler_tile_smem_bytes(int flat, int w);
+
 } // namespace s1d

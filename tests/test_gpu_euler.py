@@ -1,0 +1,110 @@
+"""GPU parity: Euler Sod (lengthening and flattening), classic and swept, vs
+the CPU oracle bit for bit (test_decomp.cpp:81-145, SURVEY.md §8c
+fingerprints), plus the device-side NonPhysicalState contract."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+import paper_1811_08282_b200 as s1d
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "golden.json")))
+METHODS = {"lengthening": s1d.Method.Lengthening, "flattening": s1d.Method.Flattening}
+
+
+def cfg(method, scheme, n, w, steps, ranks=1, wf=0, **kw):
+    return s1d.LaunchConfig(equation=s1d.Equation.Euler, method=METHODS[method], scheme=scheme, grid_size=n,
+                            block_width=w, ranks=ranks, work_factor=wf, steps=steps, **kw)
+
+
+def bits(a):
+    return np.ascontiguousarray(a, dtype=np.float64).view(np.uint64)
+
+
+def assert_bitwise(got, want):
+    assert got.shape == want.shape
+    bad = np.nonzero(bits(got) != bits(want))[0]
+    assert bad.size == 0, f"{bad.size} mismatches, first at {bad[:6]}: got {got[bad[:3]]} want {want[bad[:3]]}"
+
+
+SCHEMES = [s1d.Scheme.Swept, s1d.Scheme.Classic]
+
+
+@pytest.mark.parametrize("scheme", SCHEMES, ids=s1d.to_string)
+@pytest.mark.parametrize("fp", [f for f in GOLD["fingerprints"] if f["equation"] == "euler"],
+                         ids=lambda f: f"{f['method']}-{f['n']}-{f['steps']}")
+def test_fingerprints(gpu, scheme, fp):
+    res = s1d.run(cfg(fp["method"], scheme, fp["n"], 64, fp["steps"]))
+    assert O.fnv1a64(res.state) == fp["fnv1a64"]
+
+
+@pytest.mark.parametrize("scheme", SCHEMES, ids=s1d.to_string)
+@pytest.mark.parametrize("c", [c for c in GOLD["decomp"] if c["equation"] == "euler"],
+                         ids=lambda c: f"{c['method']}-n{c['n']}-w{c['w']}-r{c['ranks']}-T{c['steps']}")
+def test_decomp_cases(gpu, scheme, c):
+    want = np.array(c["state"])
+    for r, wf in ((c["ranks"], c["wf"]), (1, 0)):
+        res = s1d.run(cfg(c["method"], scheme, c["n"], c["w"], c["steps"], ranks=r, wf=wf))
+        assert_bitwise(res.state, want)
+        if scheme == s1d.Scheme.Swept and r == c["ranks"] and wf == c["wf"]:
+            assert res.stats.exchange_rounds == c["swept_rounds"]
+            assert res.stats.messages_sent == c["swept_messages"]
+            assert res.stats.bytes_sent == c["swept_bytes"]
+        if scheme == s1d.Scheme.Classic and r == c["ranks"] and wf == c["wf"]:
+            assert res.stats.exchange_rounds == c["classic_rounds"]
+            assert res.stats.messages_sent == c["classic_messages"]
+            assert res.stats.bytes_sent == c["classic_bytes"]
+
+
+@pytest.mark.parametrize("method", ["lengthening", "flattening"])
+@pytest.mark.parametrize("w", [8, 12, 16, 32, 64, 128, 256, 512, 1024])
+def test_width_sweep_unaligned(gpu, method, w):
+    h = 1 if method == "lengthening" else 2
+    S = 4 if method == "lengthening" else 2
+    m = w // (2 * h)
+    n = max(4 * w, 2048)
+    n -= n % w
+    for total in (m - 1, m, 2 * m, 3 * m + 3):
+        steps = max(1, total // S)
+        want = O.port_run_serial("euler", method, n=n, steps=steps)
+        got = s1d.run(cfg(method, s1d.Scheme.Swept, n, w, steps)).state
+        assert_bitwise(got, want)
+
+
+def test_flattening_equals_lengthening(gpu):
+    a = s1d.run(cfg("lengthening", s1d.Scheme.Swept, 4096, 64, 300)).state
+    b = s1d.run(cfg("flattening", s1d.Scheme.Swept, 4096, 64, 300)).state
+    assert_bitwise(a, b)
+
+
+def test_long_run_conserves_mass(gpu):
+    res = s1d.run(cfg("lengthening", s1d.Scheme.Swept, 1024, 32, 4000))
+    ic = O.port_initial_condition("euler-sod-periodic", 1024, "euler")
+    for v in range(3):
+        assert abs(res.state[v::3].sum() - ic[v::3].sum()) <= 1e-12 * max(np.abs(ic[v::3]).sum(), 1.0)
+    assert_bitwise(res.state, O.port_run_serial("euler", "lengthening", n=1024, steps=4000))
+
+
+@pytest.mark.parametrize("method", ["lengthening", "flattening"])
+@pytest.mark.parametrize("scheme", SCHEMES, ids=s1d.to_string)
+def test_nonphysical_state_raises(gpu, method, scheme):
+    # negative pressure somewhere inside the domain (test_kernels.cpp:251-255 at engine level)
+    n = 512
+    state = O.port_initial_condition("euler-sod-periodic", n, "euler")
+    state[3 * 200 + 2] = -1.0
+    with s1d.Solver(cfg(method, scheme, n, 32, 10)) as sv:
+        with pytest.raises(s1d.NonPhysicalState):
+            sv.solve(state)
+        # a good state afterwards runs clean (flag is reset per run)
+        good, _, _ = sv.solve()
+    assert_bitwise(good, O.port_run_serial("euler", method, n=n, steps=10))
+
+
+def test_uniform_is_fixed_point(gpu):
+    for method in ("lengthening", "flattening"):
+        res = s1d.run(cfg(method, s1d.Scheme.Swept, 256, 16, 25, initial="uniform"))
+        ic = O.port_initial_condition("uniform", 256, "euler")
+        assert_bitwise(res.state, ic)
