@@ -10,7 +10,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_lib", "libswept1d.so")
+LIB_PATH = os.environ.get("S1D_LIB_PATH") or os.path.join(HERE, "_lib", "libswept1d.so")
 
 S1D_HEAT, S1D_EULER = 0, 1
 S1D_LENGTHENING, S1D_FLATTENING = 0, 1

@@ -22,6 +22,7 @@
 //     onto exactly the points of the level's span (no wasted or speculative
 //     arithmetic, so the non-physical-state flag is exact).
 #include <cstdint>
+#include <cstdlib>
 
 #include "euler_math.cuh"
 #include "kernels.hpp"
@@ -30,6 +31,15 @@ namespace s1d {
 namespace {
 
 constexpr int kClassicB = 256; // points per CTA in the classic kernels
+// 4 resident CTAs of 256 threads per SM (<= 64 registers): the FP64
+// div/sqrt chains of the flux are latency-bound, so occupancy beats the
+// few bytes of spill this costs (measured: +8% swept, +20% classic).
+#ifndef S1D_EULER_MINB
+#define S1D_EULER_MINB 4
+#endif
+#ifndef S1D_EULER_CLASSIC_MINB
+#define S1D_EULER_CLASSIC_MINB 4
+#endif
 
 struct Fields {
     double* st;
@@ -59,7 +69,7 @@ __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
 // Q1, 0 corrector).
 // ---------------------------------------------------------------------------
 template <int KIND>
-__global__ void __launch_bounds__(kClassicB) euler_len_classic(const ClassicArgs a) {
+__global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_len_classic(const ClassicArgs a) {
     __shared__ double sh[3][kClassicB + 2];
     const Fields F = fields_of(a);
     const double gamma = a.gamma;
@@ -105,7 +115,7 @@ __global__ void __launch_bounds__(kClassicB) euler_len_classic(const ClassicArgs
 
 // classic, flattening. FIN = 0 predictor (Q1 <- from Q0), 1 corrector.
 template <int FIN>
-__global__ void __launch_bounds__(kClassicB) euler_flat_classic(const ClassicArgs a) {
+__global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_flat_classic(const ClassicArgs a) {
     __shared__ double sp[kClassicB + 4];
     __shared__ double sf[3][kClassicB + 1];
     const Fields F = fields_of(a);
@@ -173,7 +183,7 @@ inline std::size_t euler_tile_smem(int flat, int w) {
 }
 
 template <int FLAT, int KIND>
-__global__ void __launch_bounds__(256) euler_tile(const TileArgs a) {
+__global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs a) {
     using G = TileGeom<FLAT>;
     constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
     extern __shared__ double sm[];
@@ -358,8 +368,12 @@ cudaError_t launch_tile_f(int kind, const TileArgs& a, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
+    // narrow tiles: 128-thread CTAs (more tiles in flight per SM)
+    int cap = a.w <= 256 ? 128 : 256;
+    if (const char* e = std::getenv("S1D_EULER_NT")) cap = std::atoi(e);
+    if (cap < 32 || cap > 256) cap = 256;
     int nt = ((a.w + 2 * TileGeom<FLAT>::H + 31) / 32) * 32;
-    if (nt > 256) nt = 256;
+    if (nt > cap) nt = cap;
     if (nt < 2 * TileGeom<FLAT>::CHUNKS) nt = 32 * ((2 * TileGeom<FLAT>::CHUNKS + 31) / 32);
     k<<<a.nb, nt, smem, st>>>(a);
     return cudaGetLastError();
