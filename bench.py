@@ -267,6 +267,9 @@ def run_b200(args, rank, world):
                     "peak_source": "measured in-run: s1d_measure_fp64_peak (DADD/DMUL microkernel)",
                     "flops_per_update": HEAT_FLOPS_PER_UPDATE,
                     "updates_per_launch": dom_upd // max(dom_launch, 1),
+                    "algorithmic_dram_bytes_per_launch": 32 * n_per if dom_name == "swept_diamond" else None,
+                    "traffic_note": "traffic = ncu dram read+write bytes per Diamond launch (profiles/traffic.json); "
+                                    "algorithmic = the tiles' edge records in + out (4 doubles per point)",
                     "avg_launch_ms": round(1e3 * dom_s / max(dom_launch, 1), 4)}
         hbm = peaks.get("hbm_gbs")
         eq_gbs = CLASSIC_BYTES_PER_UPDATE * dom_upd / dom_s / 1e9
