@@ -204,12 +204,18 @@ def run_b200(args, rank, world):
     n_per = 1 << args.log2n
     eq = s1d.Equation.Heat if args.equation == "heat" else s1d.Equation.Euler
     scheme = s1d.Scheme.Swept if args.scheme == "swept" else s1d.Scheme.Classic
-    if world > 1:
-        raise SystemExit("bench.py: multi-process sharding not wired yet in this build")
-    cfg = s1d.LaunchConfig(equation=eq, scheme=scheme, grid_size=n_per, block_width=args.w, ranks=1,
-                           steps=args.T, num_devices=1)
     n_total = n_per * world
-    solver = s1d.Solver(cfg)
+    if world > 1:
+        # One process per GPU: this rank owns shard `rank` of the ring; the
+        # neighbours' boundary edges are read in place over NVLink.
+        from paper_1811_08282_b200.dist import open_ring_shard
+        cfg = s1d.LaunchConfig(equation=eq, scheme=scheme, grid_size=n_total, block_width=args.w, ranks=world,
+                               steps=args.T)
+        solver = open_ring_shard(cfg, rank, world, local)
+    else:
+        cfg = s1d.LaunchConfig(equation=eq, scheme=scheme, grid_size=n_per, block_width=args.w, ranks=1,
+                               steps=args.T, num_devices=1)
+        solver = s1d.Solver(cfg)
     # warm-up
     for _ in range(args.warmup):
         solver.advance()
@@ -238,8 +244,8 @@ def run_b200(args, rank, world):
         import torch
         hin = torch.empty(n_per, dtype=torch.float64, pin_memory=True)
         hout = torch.empty(n_per, dtype=torch.float64, pin_memory=True)
-        ic = s1d.initial_condition(cfg.initial_or_default(), n_per, cfg.spec(), cfg.phys.gamma)
-        hin.numpy()[:] = ic
+        s1d.initial_condition_range(cfg.initial_or_default(), n_total, cfg.spec(), solver.start, solver.count,
+                                    cfg.phys.gamma, out=hin.numpy())
         solver.solve_ptr(hin.data_ptr(), n_per, hout.data_ptr(), n_per)  # warm
         e2e_times = []
         for _ in range(args.e2e_steps):
@@ -281,7 +287,7 @@ def run_b200(args, rank, world):
 
     # Classic comparison on the same grid (the metric is swept vs classic).
     classic = None
-    if args.compare_classic and scheme == s1d.Scheme.Swept:
+    if args.compare_classic and scheme == s1d.Scheme.Swept and world == 1:
         ccfg = s1d.LaunchConfig(equation=eq, scheme=s1d.Scheme.Classic, grid_size=n_per, block_width=args.w,
                                 ranks=1, steps=args.classic_T, num_devices=1)
         with s1d.Solver(ccfg) as cs:

@@ -135,6 +135,9 @@ int s1d_finalize(s1d_config* cfg, int partitioned, char* err, size_t errlen);
 void s1d_spec(int equation, int method, int* substeps, int* half_width, int* slots, int* values_per_point);
 int s1d_initial_condition(const char* id, uint64_t n, int equation, double gamma, double* out, size_t out_len,
                           char* err, size_t errlen);
+/* Points [j0, j0+count) of the same initial condition (no full-grid array). */
+int s1d_initial_condition_range(const char* id, uint64_t n, int equation, double gamma, uint64_t j0, uint64_t count,
+                                double* out, size_t out_len, char* err, size_t errlen);
 int s1d_max_signal_speed(const double* prim, size_t len, double gamma, double* out, char* err, size_t errlen);
 /* arrays of length cfg->ranks */
 int s1d_partition(const s1d_config* cfg, uint64_t* blocks, uint64_t* start_index, int* left, int* right,
@@ -172,6 +175,22 @@ int s1d_read_state(s1d_solver* s, double* host_out, size_t len);
 int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_out, size_t out_len,
               s1d_stats* stats, s1d_timing* timing);
 const char* s1d_last_error(const s1d_solver* s);
+
+/* ---- one process per GPU (e.g. under torchrun) -------------------------- */
+/* Create shard `rank` (0 <= rank < cfg->ranks, partition as s1d_partition) on
+ * visible device `device`. The process owns only that shard; its ring
+ * neighbours live in other processes. Host I/O of the handle (set_initial,
+ * solve, read_state) covers the local slice [start, start+count) only. */
+int s1d_shard_create(const s1d_config* cfg, int rank, int device, s1d_solver** out, char* err, size_t errlen);
+/* Size of the opaque blob (CUDA IPC handles of the shard's device buffers). */
+size_t s1d_shard_blob_size(void);
+int s1d_shard_export(s1d_solver* s, void* blob, size_t blob_len);
+/* Map the ring neighbours' buffers (their blobs, exchanged by the caller's
+ * transport). Afterwards every s1d_advance runs in lockstep with them:
+ * boundary tiles read the neighbour's edges in place over NVLink, rounds are
+ * ordered by device-side flags (no host round trip). */
+int s1d_shard_connect(s1d_solver* s, const void* left_blob, const void* right_blob);
+int s1d_shard_range(const s1d_solver* s, uint64_t* start, uint64_t* count);
 
 /* ---- measurement helpers (not part of the reference interface) --------- */
 /* Sustained FP64 DADD/DMUL instruction rate of `device` (ops/s), measured by

@@ -7,8 +7,8 @@ this package is its Python mirror of the reference interface (api.py).
 from .api import (  # noqa: F401
     ArrayExtents, CommStats, CudaError, DegenerateFit, EngineTiming, Equation, EquationSpec, InvalidConfig,
     InvalidWidth, LaunchConfig, Method, Mode, ModeMismatch, NoDevice, NonPhysicalState, Partition,
-    PayloadSizeMismatch, PeerUnavailable, PhaseSchedule, PhaseSkew, PhysParams, RunResult, Scheme, Solver,
+    PayloadSizeMismatch, PeerUnavailable, PhaseSchedule, PhaseSkew, PhysParams, RunResult, Scheme, Shard, Solver,
     SpanAtLevel, Sweep1dError, TagMismatch, TransportAborted, TransportParams, UnknownInitialCondition,
     apply_config_entry, apply_config_file, cycle_advance, device_count, diamond_schedule, down_triangle_schedule,
-    initial_condition, make_partition, make_spec, max_signal_speed, measure_fp64_peak, run, swept_buffer_cells, to_string,
+    initial_condition, initial_condition_range, make_partition, make_spec, max_signal_speed, measure_fp64_peak, run, swept_buffer_cells, to_string,
     triangle_schedule, version, working_array_extents)

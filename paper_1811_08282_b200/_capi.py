@@ -53,6 +53,8 @@ SIGNATURES = {
     "s1d_finalize": (C.c_int, [C.POINTER(s1d_config), C.c_int] + _E),
     "s1d_spec": (None, [C.c_int, C.c_int] + [C.POINTER(C.c_int)] * 4),
     "s1d_initial_condition": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.c_double, _dp, C.c_size_t] + _E),
+    "s1d_initial_condition_range": (C.c_int, [C.c_char_p, C.c_uint64, C.c_int, C.c_double, C.c_uint64, C.c_uint64,
+                                              _dp, C.c_size_t] + _E),
     "s1d_max_signal_speed": (C.c_int, [_dp, C.c_size_t, C.c_double, _dp] + _E),
     "s1d_partition": (C.c_int, [C.POINTER(s1d_config), C.POINTER(C.c_uint64), C.POINTER(C.c_uint64),
                                 C.POINTER(C.c_int), C.POINTER(C.c_int)] + _E),
@@ -72,6 +74,11 @@ SIGNATURES = {
                             C.POINTER(s1d_timing)]),
     "s1d_last_error": (C.c_char_p, [C.c_void_p]),
     "s1d_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)] + _E),
+    "s1d_shard_create": (C.c_int, [C.POINTER(s1d_config), C.c_int, C.c_int, C.POINTER(C.c_void_p)] + _E),
+    "s1d_shard_blob_size": (C.c_size_t, []),
+    "s1d_shard_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),
+    "s1d_shard_connect": (C.c_int, [C.c_void_p, C.c_char_p, C.c_char_p]),
+    "s1d_shard_range": (C.c_int, [C.c_void_p, C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
 }
 
 _lib = None

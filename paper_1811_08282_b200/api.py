@@ -314,6 +314,18 @@ def initial_condition(ident: str, n: int, spec: EquationSpec, gamma: float = 1.4
     return out
 
 
+def initial_condition_range(ident: str, n: int, spec: EquationSpec, start: int, count: int,
+                            gamma: float = 1.4, out: Optional[np.ndarray] = None) -> np.ndarray:
+    """Points [start, start+count) of initial_condition(ident, n, ...)."""
+    vpp = 1 if spec.equation == Equation.Heat else 3
+    if out is None:
+        out = np.empty(count * vpp, dtype=np.float64)
+    e = _errbuf()
+    _check(lib().s1d_initial_condition_range(ident.encode(), n, int(spec.equation), gamma, start, count,
+                                             out.ctypes.data_as(C.POINTER(C.c_double)), out.size, e, 1024), e)
+    return out
+
+
 def max_signal_speed(primaries: np.ndarray, gamma: float) -> float:
     a = np.ascontiguousarray(primaries, dtype=np.float64)
     out = C.c_double()
@@ -437,11 +449,17 @@ class Solver:
         self._h = C.c_void_p()
         e = _errbuf()
         _check(lib().s1d_create(C.byref(cfg.to_c()), C.byref(self._h), e, 1024), e)
+        self._post_init()
+
+    def _post_init(self):
         c = _capi.s1d_config()
         lib().s1d_get_config(self._h, C.byref(c))
         self.cfg = LaunchConfig.from_c(c)
         self.spec = self.cfg.spec()
-        self.state_len = self.cfg.grid_size * self.spec.values_per_point
+        start, count = C.c_uint64(), C.c_uint64()
+        lib().s1d_shard_range(self._h, C.byref(start), C.byref(count))
+        self.start, self.count = start.value, count.value
+        self.state_len = self.count * self.spec.values_per_point
 
     def _chk(self, status: int):
         if status:
@@ -500,6 +518,33 @@ class Solver:
             status = lib().s1d_solve(self._h, None, 0, _dptr(out), out.size, C.byref(st), C.byref(tm))
         self._chk(status)
         return out, _stats(st), _timing(tm)
+
+
+class Shard(Solver):
+    """One shard of the ring owned by this process (one process per GPU).
+
+    Usage (e.g. under torchrun):
+        sh = Shard(cfg, rank, device)
+        blobs = all_gather(sh.export())            # any transport
+        sh.connect(blobs[left], blobs[right])
+        sh.advance()                               # lockstep with the neighbours
+    Host I/O covers the local slice [sh.start, sh.start + sh.count)."""
+
+    def __init__(self, cfg: LaunchConfig, rank: int, device: int):
+        self._h = C.c_void_p()
+        e = _errbuf()
+        _check(lib().s1d_shard_create(C.byref(cfg.to_c()), rank, device, C.byref(self._h), e, 1024), e)
+        self.rank = rank
+        self._post_init()
+
+    def export(self) -> bytes:
+        n = lib().s1d_shard_blob_size()
+        buf = C.create_string_buffer(n)
+        self._chk(lib().s1d_shard_export(self._h, buf, n))
+        return buf.raw
+
+    def connect(self, left_blob: bytes, right_blob: bytes) -> None:
+        self._chk(lib().s1d_shard_connect(self._h, left_blob, right_blob))
 
 
 def measure_fp64_peak(device: int = 0) -> float:

@@ -41,6 +41,7 @@ struct CudaError : Error {
     } while (0)
 
 struct Shard {
+    bool local = true;        // false: a view of a neighbour shard owned by another process
     int dev = 0;
     cudaStream_t st = nullptr;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_done = nullptr;
@@ -51,10 +52,25 @@ struct Shard {
     double* state[2] = {nullptr, nullptr};
     double* EL[2] = {nullptr, nullptr};
     double* ER[2] = {nullptr, nullptr};
+    unsigned* flags = nullptr; // multi-process: [0] left neighbour's rounds, [1] right's
     int* err = nullptr;
     double* staging = nullptr; // AoS (vpp = 3) upload/download buffer (Euler)
     const double* final_state = nullptr;
 };
+
+// Fixed-size description of a shard's device buffers for CUDA IPC.
+struct ShardBlob {
+    std::uint32_t magic = 0x53314442u; // "S1DB"
+    std::uint32_t version = 1;
+    std::int32_t rank = -1;
+    std::int32_t nhandles = 0;
+    std::uint64_t N = 0, nb = 0, start = 0, fstride = 0;
+    std::uint32_t present = 0; // bit k: handle k valid
+    std::uint32_t pad = 0;
+    cudaIpcMemHandle_t h[8];   // ic, state0, state1, EL0, EL1, ER0, ER1, flags
+};
+
+constexpr std::uint64_t kRoundTimeoutNs = 60ull * 1000 * 1000 * 1000; // dead-peer guard
 
 } // namespace
 
@@ -62,27 +78,40 @@ struct Solver {
     s1d_config cfg{};
     Spec spec;
     Partition part;
-    std::vector<Shard> shards;
+    std::vector<Shard> shards; // all R shards of the ring (remote ones are views in multi-process mode)
+    std::vector<int> locals;   // shards owned by this process
+    bool mp = false;           // one process per shard (IPC + device flags)
+    bool connected = false;
+    unsigned seq = 0;          // rounds completed by this process (multi-process)
+    std::vector<void*> ipc_open;
     int ndev = 1;
     std::uint64_t m = 0;
     int p = 2;
     bool euler = false, flat = false;
     double setup_seconds = 0.0;
     std::string last_error;
-    std::vector<double> host_ic;
+    std::vector<double> host_ic; // initial condition of the local shards (global order within)
 
     ~Solver() { release(); }
 
     void release() {
         for (auto& s : shards) {
+            if (!s.local) continue;
             cudaSetDevice(s.dev);
             if (s.st) cudaStreamSynchronize(s.st);
+        }
+        for (void* ptr : ipc_open) cudaIpcCloseMemHandle(ptr);
+        ipc_open.clear();
+        for (auto& s : shards) {
+            if (!s.local) continue;
+            cudaSetDevice(s.dev);
             cudaFree(s.ic);
             for (int k = 0; k < 2; ++k) {
                 cudaFree(s.state[k]);
                 cudaFree(s.EL[k]);
                 cudaFree(s.ER[k]);
             }
+            cudaFree(s.flags);
             cudaFree(s.err);
             cudaFree(s.staging);
             if (s.ev_start) cudaEventDestroy(s.ev_start);
@@ -93,14 +122,15 @@ struct Solver {
             if (s.st) cudaStreamDestroy(s.st);
         }
         shards.clear();
+        locals.clear();
     }
 
     Shard& left_of(int g) { return shards[static_cast<std::size_t>(part.left[static_cast<std::size_t>(g)])]; }
     Shard& right_of(int g) { return shards[static_cast<std::size_t>(part.right[static_cast<std::size_t>(g)])]; }
     int R() const { return static_cast<int>(shards.size()); }
+    Shard& sh(int g) { return shards[static_cast<std::size_t>(g)]; }
 
-    void init(const s1d_config& in) {
-        const auto t0 = std::chrono::steady_clock::now();
+    void configure(const s1d_config& in) {
         cfg = in;
         finalize(cfg, true);
         spec = make_spec(cfg.equation, cfg.method);
@@ -121,102 +151,205 @@ struct Solver {
                                                    " exceeds the shared-memory-resident Euler tile (227 KB per CTA)");
             }
         }
-
         int visible = 0;
-        if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0)
+        if (cudaGetDeviceCount(&visible) != cudaSuccess || visible == 0) {
+            cudaGetLastError();
             throw Error(S1D_NO_DEVICE, "no CUDA device visible");
+        }
         ndev = cfg.num_devices > 0 ? std::min(cfg.num_devices, visible) : visible;
         ndev = std::min(ndev, cfg.ranks);
-
-        // Peer access between ring neighbours on distinct devices.
-        for (int g = 0; g < cfg.ranks; ++g) {
-            const int d = g % ndev;
-            for (int nb : {part.left[static_cast<std::size_t>(g)], part.right[static_cast<std::size_t>(g)]}) {
-                const int dn = nb % ndev;
-                if (dn == d) continue;
-                int ok = 0;
-                S1D_CUDA(cudaDeviceCanAccessPeer(&ok, d, dn));
-                if (!ok) throw Error(S1D_PEER_UNAVAILABLE, "device " + std::to_string(d) +
-                                                               " cannot access peer " + std::to_string(dn));
-                S1D_CUDA(cudaSetDevice(d));
-                const cudaError_t e = cudaDeviceEnablePeerAccess(dn, 0);
-                if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
-                    throw CudaError(std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
-                cudaGetLastError();
-            }
-        }
-
-        host_ic = initial_condition(initial_or_default(cfg), cfg.grid_size, cfg.equation, cfg.gamma);
+        shards.assign(static_cast<std::size_t>(cfg.ranks), Shard{});
         const std::uint64_t w = cfg.block_width;
-        shards.resize(static_cast<std::size_t>(cfg.ranks));
         for (int g = 0; g < cfg.ranks; ++g) {
-            Shard& s = shards[static_cast<std::size_t>(g)];
-            s.dev = g % ndev;
+            Shard& s = sh(g);
             s.nb = part.blocks[static_cast<std::size_t>(g)];
             s.N = s.nb * w;
             s.start = part.start[static_cast<std::size_t>(g)];
             s.fstride = s.N;
-            S1D_CUDA(cudaSetDevice(s.dev));
-            S1D_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
-            S1D_CUDA(cudaEventCreate(&s.ev_start));
-            S1D_CUDA(cudaEventCreate(&s.ev_stop));
-            S1D_CUDA(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
-            S1D_CUDA(cudaEventCreate(&s.ev_dom0));
-            S1D_CUDA(cudaEventCreate(&s.ev_dom1));
-            const std::size_t state_bytes = sizeof(double) * s.N * static_cast<std::size_t>(spec.rec);
-            S1D_CUDA(cudaMalloc(&s.ic, state_bytes));
-            S1D_CUDA(cudaMalloc(&s.state[0], state_bytes));
-            S1D_CUDA(cudaMalloc(&s.state[1], state_bytes));
-            S1D_CUDA(cudaMalloc(&s.err, sizeof(int)));
-            S1D_CUDA(cudaMemset(s.err, 0, sizeof(int)));
-            if (euler) S1D_CUDA(cudaMalloc(&s.staging, sizeof(double) * 3 * s.N));
-            if (cfg.scheme == S1D_SWEPT) {
-                const std::size_t edge_bytes = sizeof(double) * s.nb * w * static_cast<std::size_t>(spec.rec);
-                for (int k = 0; k < 2; ++k) {
-                    S1D_CUDA(cudaMalloc(&s.EL[k], edge_bytes));
-                    S1D_CUDA(cudaMalloc(&s.ER[k], edge_bytes));
-                }
+        }
+    }
+
+    void allocate(Shard& s) {
+        const std::uint64_t w = cfg.block_width;
+        S1D_CUDA(cudaSetDevice(s.dev));
+        S1D_CUDA(cudaStreamCreateWithFlags(&s.st, cudaStreamNonBlocking));
+        S1D_CUDA(cudaEventCreate(&s.ev_start));
+        S1D_CUDA(cudaEventCreate(&s.ev_stop));
+        S1D_CUDA(cudaEventCreateWithFlags(&s.ev_done, cudaEventDisableTiming));
+        S1D_CUDA(cudaEventCreate(&s.ev_dom0));
+        S1D_CUDA(cudaEventCreate(&s.ev_dom1));
+        const std::size_t state_bytes = sizeof(double) * s.N * static_cast<std::size_t>(spec.rec);
+        S1D_CUDA(cudaMalloc(&s.ic, state_bytes));
+        S1D_CUDA(cudaMalloc(&s.state[0], state_bytes));
+        S1D_CUDA(cudaMalloc(&s.state[1], state_bytes));
+        S1D_CUDA(cudaMalloc(&s.err, sizeof(int)));
+        S1D_CUDA(cudaMemset(s.err, 0, sizeof(int)));
+        if (euler) S1D_CUDA(cudaMalloc(&s.staging, sizeof(double) * 3 * s.N));
+        if (cfg.scheme == S1D_SWEPT) {
+            const std::size_t edge_bytes = sizeof(double) * s.nb * w * static_cast<std::size_t>(spec.rec);
+            for (int k = 0; k < 2; ++k) {
+                S1D_CUDA(cudaMalloc(&s.EL[k], edge_bytes));
+                S1D_CUDA(cudaMalloc(&s.ER[k], edge_bytes));
             }
         }
-        upload(host_ic.data());
+        if (mp) {
+            S1D_CUDA(cudaMalloc(&s.flags, 256));
+            S1D_CUDA(cudaMemset(s.flags, 0, 256));
+        }
+    }
+
+    void enable_peer(int d, int dn) {
+        if (d == dn) return;
+        int ok = 0;
+        S1D_CUDA(cudaDeviceCanAccessPeer(&ok, d, dn));
+        if (!ok)
+            throw Error(S1D_PEER_UNAVAILABLE,
+                        "device " + std::to_string(d) + " cannot access peer " + std::to_string(dn));
+        S1D_CUDA(cudaSetDevice(d));
+        const cudaError_t e = cudaDeviceEnablePeerAccess(dn, 0);
+        if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+            throw CudaError(std::string("cudaDeviceEnablePeerAccess: ") + cudaGetErrorString(e));
+        cudaGetLastError();
+    }
+
+    // Single process: every shard local, shard g on device g % ndev.
+    void init(const s1d_config& in) {
+        const auto t0 = std::chrono::steady_clock::now();
+        configure(in);
+        for (int g = 0; g < R(); ++g) {
+            sh(g).dev = g % ndev;
+            locals.push_back(g);
+        }
+        for (int g = 0; g < R(); ++g) {
+            enable_peer(sh(g).dev, left_of(g).dev);
+            enable_peer(sh(g).dev, right_of(g).dev);
+        }
+        for (int g : locals) allocate(sh(g));
+        connected = true;
+        host_ic = initial_condition(initial_or_default(cfg), cfg.grid_size, cfg.equation, cfg.gamma);
+        upload(host_ic.data(), false);
         sync_all();
         setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     }
 
+    // Multi-process: this process owns shard `rank` on `device`.
+    void init_shard(const s1d_config& in, int rank, int device) {
+        const auto t0 = std::chrono::steady_clock::now();
+        configure(in);
+        if (rank < 0 || rank >= R()) throw Error(S1D_INVALID_CONFIG, "shard rank out of range");
+        int visible = 0;
+        cudaGetDeviceCount(&visible);
+        if (device < 0 || device >= visible) throw Error(S1D_NO_DEVICE, "device index out of range");
+        mp = R() > 1;
+        for (auto& s : shards) s.local = false;
+        Shard& me = sh(rank);
+        me.local = true;
+        me.dev = device;
+        locals.push_back(rank);
+        allocate(me);
+        connected = R() == 1;
+        host_ic = initial_condition_range(initial_or_default(cfg), cfg.grid_size, cfg.equation, cfg.gamma, me.start,
+                                          me.N);
+        upload(host_ic.data(), true);
+        sync_all();
+        setup_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    }
+
+    void export_blob(ShardBlob* b) {
+        if (locals.size() != 1) throw Error(S1D_INVALID_CONFIG, "export needs a single-shard (multi-process) solver");
+        Shard& s = sh(locals[0]);
+        *b = ShardBlob{};
+        b->rank = locals[0];
+        b->N = s.N;
+        b->nb = s.nb;
+        b->start = s.start;
+        b->fstride = s.fstride;
+        void* ptrs[8] = {s.ic, s.state[0], s.state[1], s.EL[0], s.EL[1], s.ER[0], s.ER[1], s.flags};
+        S1D_CUDA(cudaSetDevice(s.dev));
+        for (int k = 0; k < 8; ++k) {
+            if (!ptrs[k]) continue;
+            S1D_CUDA(cudaIpcGetMemHandle(&b->h[k], ptrs[k]));
+            b->present |= 1u << k;
+        }
+        b->nhandles = 8;
+    }
+
+    void open_view(const ShardBlob& b) {
+        if (b.magic != 0x53314442u || b.version != 1) throw Error(S1D_INVALID_CONFIG, "bad shard blob");
+        if (b.rank < 0 || b.rank >= R()) throw Error(S1D_INVALID_CONFIG, "shard blob rank out of range");
+        Shard& v = sh(b.rank);
+        if (v.local || v.ic) return; // own shard, or already opened (R == 2: left == right)
+        if (v.N != b.N || v.start != b.start)
+            throw Error(S1D_INVALID_CONFIG, "shard blob does not match this configuration's partition");
+        void** dst[8] = {reinterpret_cast<void**>(&v.ic), reinterpret_cast<void**>(&v.state[0]),
+                         reinterpret_cast<void**>(&v.state[1]), reinterpret_cast<void**>(&v.EL[0]),
+                         reinterpret_cast<void**>(&v.EL[1]), reinterpret_cast<void**>(&v.ER[0]),
+                         reinterpret_cast<void**>(&v.ER[1]), reinterpret_cast<void**>(&v.flags)};
+        S1D_CUDA(cudaSetDevice(sh(locals[0]).dev));
+        for (int k = 0; k < 8; ++k) {
+            if (!(b.present & (1u << k))) continue;
+            void* ptr = nullptr;
+            const cudaError_t e = cudaIpcOpenMemHandle(&ptr, b.h[k], cudaIpcMemLazyEnablePeerAccess);
+            if (e != cudaSuccess)
+                throw Error(S1D_PEER_UNAVAILABLE, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+            ipc_open.push_back(ptr);
+            *dst[k] = ptr;
+        }
+        v.fstride = b.fstride;
+        v.nb = b.nb;
+    }
+
+    void connect(const ShardBlob* left, const ShardBlob* right) {
+        if (locals.size() != 1) throw Error(S1D_INVALID_CONFIG, "connect needs a multi-process shard solver");
+        const int me = locals[0];
+        if (R() == 1) {
+            connected = true;
+            return;
+        }
+        if (left->rank != part.left[static_cast<std::size_t>(me)] ||
+            right->rank != part.right[static_cast<std::size_t>(me)])
+            throw Error(S1D_INVALID_CONFIG, "connect: blobs are not this shard's ring neighbours");
+        open_view(*left);
+        open_view(*right);
+        connected = true;
+    }
+
     void sync_all() {
-        for (auto& s : shards) {
-            S1D_CUDA(cudaSetDevice(s.dev));
-            S1D_CUDA(cudaStreamSynchronize(s.st));
+        for (int g : locals) {
+            S1D_CUDA(cudaSetDevice(sh(g).dev));
+            S1D_CUDA(cudaStreamSynchronize(sh(g).st));
         }
     }
 
-    // Global-order host state (vpp doubles per point) -> per-shard SoA ic
-    // (Euler: make_cell, Q0 = Q1 = v, Pr = 0; inc/kernels.hpp:144-149).
-    void upload(const double* host) {
-        for (auto& s : shards) {
+    // Host state -> per-shard SoA ic (Euler: make_cell, Q0 = Q1 = v, Pr = 0;
+    // inc/kernels.hpp:144-149). local_slice: `host` holds only the local
+    // shard's points (multi-process), else the global array.
+    void upload(const double* host, bool local_slice) {
+        for (int g : locals) {
+            Shard& s = sh(g);
+            const double* src = host + (local_slice ? 0 : s.start * spec.vpp);
             S1D_CUDA(cudaSetDevice(s.dev));
             if (!euler) {
-                S1D_CUDA(cudaMemcpyAsync(s.ic, host + s.start, sizeof(double) * s.N, cudaMemcpyHostToDevice, s.st));
+                S1D_CUDA(cudaMemcpyAsync(s.ic, src, sizeof(double) * s.N, cudaMemcpyHostToDevice, s.st));
             } else {
-                S1D_CUDA(cudaMemcpyAsync(s.staging, host + 3 * s.start, sizeof(double) * 3 * s.N,
-                                         cudaMemcpyHostToDevice, s.st));
+                S1D_CUDA(cudaMemcpyAsync(s.staging, src, sizeof(double) * 3 * s.N, cudaMemcpyHostToDevice, s.st));
                 S1D_CUDA(launch_euler_unpack(s.staging, s.ic, s.N, s.fstride, spec.rec, s.st));
             }
         }
     }
 
-    // Final state -> global-order host array (extract: Q0 for Euler,
-    // inc/kernels.hpp:150-154; the current level for heat).
-    void download(double* host) {
-        for (auto& s : shards) {
+    // Final state -> host (extract: Q0 for Euler, inc/kernels.hpp:150-154;
+    // the current level for heat).
+    void download(double* host, bool local_slice) {
+        for (int g : locals) {
+            Shard& s = sh(g);
+            double* dst = host + (local_slice ? 0 : s.start * spec.vpp);
             S1D_CUDA(cudaSetDevice(s.dev));
             if (!euler) {
-                S1D_CUDA(cudaMemcpyAsync(host + s.start, s.final_state, sizeof(double) * s.N,
-                                         cudaMemcpyDeviceToHost, s.st));
+                S1D_CUDA(cudaMemcpyAsync(dst, s.final_state, sizeof(double) * s.N, cudaMemcpyDeviceToHost, s.st));
             } else {
                 S1D_CUDA(launch_euler_pack(s.final_state, s.staging, s.N, s.fstride, s.st));
-                S1D_CUDA(cudaMemcpyAsync(host + 3 * s.start, s.staging, sizeof(double) * 3 * s.N,
-                                         cudaMemcpyDeviceToHost, s.st));
+                S1D_CUDA(cudaMemcpyAsync(dst, s.staging, sizeof(double) * 3 * s.N, cudaMemcpyDeviceToHost, s.st));
             }
         }
         sync_all();
@@ -224,12 +357,19 @@ struct Solver {
 
     // Cross-shard ordering: every launch on shard g waits for the previous
     // launch of both ring neighbours (RAW on the edges/halos it reads, WAR on
-    // the buffers they read). Waits of a round are enqueued before any event
-    // of the round is re-recorded.
+    // the buffers they read). Single process: CUDA events, the waits of a
+    // round enqueued before any event of the round is re-recorded. Multi
+    // process: device flags (sync.cu).
     void wait_neighbours() {
         if (R() == 1) return;
-        for (int g = 0; g < R(); ++g) {
-            Shard& s = shards[static_cast<std::size_t>(g)];
+        if (mp) {
+            Shard& s = sh(locals[0]);
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(launch_wait_flags(s.flags, seq, s.err, kRoundTimeoutNs, s.st));
+            return;
+        }
+        for (int g : locals) {
+            Shard& s = sh(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaStreamWaitEvent(s.st, left_of(g).ev_done, 0));
             S1D_CUDA(cudaStreamWaitEvent(s.st, right_of(g).ev_done, 0));
@@ -237,40 +377,53 @@ struct Solver {
     }
     void record_round() {
         if (R() == 1) return;
-        for (auto& s : shards) {
+        if (mp) {
+            const int me = locals[0];
+            Shard& s = sh(me);
+            ++seq;
+            // I am my left neighbour's RIGHT neighbour (its flags[1]) and my
+            // right neighbour's LEFT neighbour (its flags[0]).
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(launch_signal_flags(left_of(me).flags + 1, right_of(me).flags + 0, seq, s.st));
+            return;
+        }
+        for (int g : locals) {
+            Shard& s = sh(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaEventRecord(s.ev_done, s.st));
         }
     }
 
     void record_all(cudaEvent_t Shard::*ev) {
-        for (auto& s : shards) {
+        for (int g : locals) {
+            Shard& s = sh(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaEventRecord(s.*ev, s.st));
         }
     }
 
-    void classic_steps(std::int64_t c_begin, std::int64_t c_end, const double** cur_per_shard, int* cur_idx,
+    void classic_steps(std::int64_t c_begin, std::int64_t c_end, std::vector<const double*>& cur, int* cur_idx,
                        s1d_stats& stats, bool dominant = false) {
-        // cur_per_shard[g]: buffer holding the current level; results ping-pong
-        // through state[0]/state[1] (cur_idx: which one holds the result, -1 = ic).
+        // cur[g]: buffer holding shard g's current level; heat ping-pongs
+        // through state[0]/state[1] (cur_idx: which one holds the result, -1 =
+        // ic); Euler updates state[0] in place.
         for (std::int64_t c = c_begin; c <= c_end; ++c) {
             wait_neighbours();
             if (dominant && c == c_begin) record_all(&Shard::ev_dom0);
             const int nxt = euler ? 0 : ((*cur_idx == 0) ? 1 : 0);
-            for (int g = 0; g < R(); ++g) {
-                Shard& s = shards[static_cast<std::size_t>(g)];
+            for (int g : locals) {
+                Shard& s = sh(g);
                 Shard& L = left_of(g);
                 Shard& Rt = right_of(g);
-                const double* curL = cur_per_shard[part.left[static_cast<std::size_t>(g)]];
-                const double* curR = cur_per_shard[part.right[static_cast<std::size_t>(g)]];
+                const double* curL = cur[static_cast<std::size_t>(part.left[static_cast<std::size_t>(g)])];
+                const double* curR = cur[static_cast<std::size_t>(part.right[static_cast<std::size_t>(g)])];
                 ClassicArgs a;
                 a.N = s.N;
                 a.h = spec.h;
                 a.counter = c;
                 a.fstride = s.fstride;
-                a.in = cur_per_shard[g];
-                a.out = s.state[nxt];
+                a.in = cur[static_cast<std::size_t>(g)];
+                a.out = euler ? s.state[0] : s.state[nxt];
                 a.halo_l = curL + (L.N - static_cast<std::uint64_t>(spec.h));
                 a.halo_r = curR;
                 a.halo_l_fstride = L.fstride;
@@ -280,19 +433,14 @@ struct Solver {
                 a.dt_dx = cfg.dt_dx;
                 a.error_flag = s.err;
                 S1D_CUDA(cudaSetDevice(s.dev));
-                if (euler) {
-                    // in place on state[0] (cur == state[0] for every shard)
-                    a.out = s.state[0];
-                    S1D_CUDA(launch_euler_classic(flat ? 1 : 0, a, s.st));
-                } else {
-                    S1D_CUDA(launch_heat_classic(a, s.st));
-                }
+                if (euler) S1D_CUDA(launch_euler_classic(flat ? 1 : 0, a, s.st));
+                else S1D_CUDA(launch_heat_classic(a, s.st));
                 stats.kernel_launches += 1;
             }
             if (dominant && c == c_end) record_all(&Shard::ev_dom1);
             record_round();
             *cur_idx = nxt;
-            for (int g = 0; g < R(); ++g) cur_per_shard[g] = shards[static_cast<std::size_t>(g)].state[nxt];
+            for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).state[nxt];
         }
     }
 
@@ -301,8 +449,8 @@ struct Solver {
         if (dom_first) record_all(&Shard::ev_dom0);
         const int w = static_cast<int>(cfg.block_width);
         const int src = static_cast<int>((j + 1) & 1), dst = static_cast<int>(j & 1);
-        for (int g = 0; g < R(); ++g) {
-            Shard& s = shards[static_cast<std::size_t>(g)];
+        for (int g : locals) {
+            Shard& s = sh(g);
             Shard& L = left_of(g);
             Shard& Rt = right_of(g);
             TileArgs a;
@@ -342,13 +490,15 @@ struct Solver {
     }
 
     void advance(s1d_stats* stats_out, s1d_timing* timing_out) {
+        if (!connected) throw Error(S1D_INVALID_CONFIG, "shard not connected: call s1d_shard_connect first");
         s1d_stats stats{};
         const std::int64_t total = cfg.steps * spec.S;
         const std::int64_t cycles = cfg.scheme == S1D_SWEPT ? total / static_cast<std::int64_t>(m) : 0;
         const std::int64_t pad = total - cycles * static_cast<std::int64_t>(m);
 
         sync_all();
-        for (auto& s : shards) {
+        for (int g : locals) {
+            Shard& s = sh(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaMemsetAsync(s.err, 0, sizeof(int), s.st));
             // Euler classic substeps run in place on state[0]; seed it with the
@@ -359,11 +509,11 @@ struct Solver {
                                          s.st));
             S1D_CUDA(cudaEventRecord(s.ev_start, s.st));
         }
-        record_round();
+        record_round(); // "initial state resident" round
 
         std::vector<const double*> cur(static_cast<std::size_t>(R()));
         int cur_idx = -1;
-        for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].ic;
+        for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).ic;
         // Dominant kernel: the Diamond phases when there are any, else the
         // classic substeps, else the Up/Down pair.
         const bool dom_diamond = cycles >= 2;
@@ -375,18 +525,21 @@ struct Solver {
                 swept_phase(j == cycles ? kDown : kDiamond, j, stats, dom_diamond && j == 1,
                             (dom_diamond && j == cycles - 1) || (dom_updown && j == cycles));
             cur_idx = 0;
-            for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].state[0];
+            for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).state[0];
         }
         if (pad > 0) {
             if (euler && cycles == 0) {
                 cur_idx = 0;
-                for (int g = 0; g < R(); ++g)
-                    cur[static_cast<std::size_t>(g)] = shards[static_cast<std::size_t>(g)].state[0];
+                for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).state[0];
             }
-            classic_steps(cycles * static_cast<std::int64_t>(m) + 1, total, cur.data(), &cur_idx, stats, dom_classic);
+            classic_steps(cycles * static_cast<std::int64_t>(m) + 1, total, cur, &cur_idx, stats, dom_classic);
         }
+        // The left neighbour's last Down tile writes into this shard's state:
+        // make its completion part of this shard's run.
+        if (mp) wait_neighbours();
 
-        for (auto& s : shards) {
+        for (int g : locals) {
+            Shard& s = sh(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaEventRecord(s.ev_stop, s.st));
         }
@@ -394,8 +547,8 @@ struct Solver {
         float worst_ms = 0.0f, dom_ms = 0.0f;
         const bool have_dom = dom_diamond || dom_classic || dom_updown;
         int flag = 0;
-        for (int g = 0; g < R(); ++g) {
-            Shard& s = shards[static_cast<std::size_t>(g)];
+        for (int g : locals) {
+            Shard& s = sh(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             float ms = 0.0f;
             S1D_CUDA(cudaEventElapsedTime(&ms, s.ev_start, s.ev_stop));
@@ -410,6 +563,7 @@ struct Solver {
             s.final_state = cur[static_cast<std::size_t>(g)];
         }
         S1D_CUDA(cudaGetLastError());
+        if (flag & 2) throw Error(S1D_TRANSPORT_ABORTED, "a neighbour shard stopped responding (round timeout)");
         if (flag) throw Error(S1D_NONPHYSICAL, "non-physical state encountered on the device");
 
         // Reference accounting (transport.cpp:48-110): a swept cycle is one
@@ -423,7 +577,7 @@ struct Solver {
         stats.bytes_sent = Rn * (static_cast<std::uint64_t>(cycles) * buf * cell +
                                  static_cast<std::uint64_t>(pad) * 2 * static_cast<std::uint64_t>(spec.h) * cell);
         if (Rn > 1)
-            stats.edge_bytes_device += static_cast<std::uint64_t>(pad) * Rn * 2 * sizeof(double) *
+            stats.edge_bytes_device += static_cast<std::uint64_t>(pad) * locals.size() * 2 * sizeof(double) *
                                        static_cast<std::uint64_t>(spec.h) * static_cast<std::uint64_t>(spec.rec);
         if (stats_out) *stats_out = stats;
         if (timing_out) {
@@ -431,25 +585,36 @@ struct Solver {
             timing_out->loop_seconds = worst_ms * 1e-3;
             timing_out->virtual_seconds = 0.0;
             timing_out->dominant_seconds = dom_ms * 1e-3;
+            std::uint64_t pts = 0;
+            for (int g : locals) pts += sh(g).N;
             const char* name = "";
             if (dom_diamond) {
                 timing_out->dominant_launches = static_cast<std::uint64_t>(cycles - 1);
-                timing_out->dominant_point_updates = static_cast<std::uint64_t>(cycles - 1) * m * cfg.grid_size;
+                timing_out->dominant_point_updates = static_cast<std::uint64_t>(cycles - 1) * m * pts;
                 name = "swept_diamond";
             } else if (dom_classic) {
                 timing_out->dominant_launches = static_cast<std::uint64_t>(pad);
-                timing_out->dominant_point_updates = static_cast<std::uint64_t>(pad) * cfg.grid_size;
+                timing_out->dominant_point_updates = static_cast<std::uint64_t>(pad) * pts;
                 name = "classic_substep";
             } else if (dom_updown) {
                 timing_out->dominant_launches = 2;
-                timing_out->dominant_point_updates = m * cfg.grid_size;
+                timing_out->dominant_point_updates = m * pts;
                 name = "swept_up_down";
             }
             std::snprintf(timing_out->dominant_kernel, sizeof(timing_out->dominant_kernel), "%s", name);
         }
     }
 
-    std::size_t state_len() const { return cfg.grid_size * static_cast<std::uint64_t>(spec.vpp); }
+    // Points (x vpp) the host I/O of this solver covers: the global array
+    // (single process) or the local shard's slice (multi-process).
+    std::size_t state_len() const {
+        std::uint64_t pts = 0;
+        if (locals.size() == shards.size()) pts = cfg.grid_size;
+        else
+            for (int g : locals) pts += shards[static_cast<std::size_t>(g)].N;
+        return pts * static_cast<std::uint64_t>(spec.vpp);
+    }
+    bool local_io() const { return locals.size() != shards.size(); }
 };
 
 } // namespace s1d
@@ -559,6 +724,16 @@ int s1d_initial_condition(const char* id, uint64_t n, int equation, double gamma
     });
 }
 
+int s1d_initial_condition_range(const char* id, uint64_t n, int equation, double gamma, uint64_t j0, uint64_t count,
+                                double* out, size_t out_len, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        if (j0 + count > n) throw s1d::Error(S1D_INVALID_CONFIG, "range outside the grid");
+        const auto v = s1d::initial_condition_range(id, n, equation, gamma, j0, count);
+        if (v.size() > out_len) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
+        std::memcpy(out, v.data(), v.size() * sizeof(double));
+    });
+}
+
 int s1d_max_signal_speed(const double* prim, size_t len, double gamma, double* out, char* err, size_t errlen) {
     return guarded(err, errlen, [&] { *out = s1d::max_signal_speed(prim, len, gamma); });
 }
@@ -617,10 +792,10 @@ int s1d_get_config(const s1d_solver* s, s1d_config* out) {
 int s1d_set_initial(s1d_solver* s, const double* host_state, size_t len) {
     return guarded_solver(s, [&] {
         if (!host_state) {
-            s->impl.upload(s->impl.host_ic.data());
+            s->impl.upload(s->impl.host_ic.data(), s->impl.local_io());
         } else {
             if (len != s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "initial state length mismatch");
-            s->impl.upload(host_state);
+            s->impl.upload(host_state, s->impl.local_io());
         }
         s->impl.sync_all();
     });
@@ -636,9 +811,9 @@ int s1d_advance(s1d_solver* s, s1d_stats* stats, s1d_timing* timing) {
 int s1d_read_state(s1d_solver* s, double* host_out, size_t len) {
     return guarded_solver(s, [&] {
         if (len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
-        for (auto& sh : s->impl.shards)
-            if (!sh.final_state) throw s1d::Error(S1D_INVALID_CONFIG, "no state: call s1d_advance first");
-        s->impl.download(host_out);
+        for (int g : s->impl.locals)
+            if (!s->impl.sh(g).final_state) throw s1d::Error(S1D_INVALID_CONFIG, "no state: call s1d_advance first");
+        s->impl.download(host_out, s->impl.local_io());
     });
 }
 
@@ -650,12 +825,12 @@ int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_
         if (out_len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
         s1d_timing t{};
         const auto t0 = std::chrono::steady_clock::now();
-        s->impl.upload(host_in ? host_in : s->impl.host_ic.data());
+        s->impl.upload(host_in ? host_in : s->impl.host_ic.data(), s->impl.local_io());
         s->impl.sync_all();
         const auto t1 = std::chrono::steady_clock::now();
         s->impl.advance(stats, &t);
         const auto t2 = std::chrono::steady_clock::now();
-        s->impl.download(host_out);
+        s->impl.download(host_out, s->impl.local_io());
         const auto t3 = std::chrono::steady_clock::now();
         t.h2d_seconds = std::chrono::duration<double>(t1 - t0).count();
         t.d2h_seconds = std::chrono::duration<double>(t3 - t2).count();
@@ -664,6 +839,41 @@ int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_
 }
 
 const char* s1d_last_error(const s1d_solver* s) { return s ? s->impl.last_error.c_str() : ""; }
+
+int s1d_shard_create(const s1d_config* cfg, int rank, int device, s1d_solver** out, char* err, size_t errlen) {
+    *out = nullptr;
+    auto holder = std::make_unique<s1d_solver>();
+    const int st = guarded(err, errlen, [&] { holder->impl.init_shard(*cfg, rank, device); });
+    if (st == S1D_OK) *out = holder.release();
+    return st;
+}
+
+size_t s1d_shard_blob_size(void) { return sizeof(s1d::ShardBlob); }
+
+int s1d_shard_export(s1d_solver* s, void* blob, size_t blob_len) {
+    return guarded_solver(s, [&] {
+        if (blob_len < sizeof(s1d::ShardBlob)) throw s1d::Error(S1D_INVALID_CONFIG, "blob buffer too small");
+        s->impl.export_blob(static_cast<s1d::ShardBlob*>(blob));
+    });
+}
+
+int s1d_shard_connect(s1d_solver* s, const void* left_blob, const void* right_blob) {
+    return guarded_solver(s, [&] {
+        s->impl.connect(static_cast<const s1d::ShardBlob*>(left_blob), static_cast<const s1d::ShardBlob*>(right_blob));
+    });
+}
+
+int s1d_shard_range(const s1d_solver* s, uint64_t* start, uint64_t* count) {
+    if (s->impl.locals.size() != 1) {
+        *start = 0;
+        *count = s->impl.cfg.grid_size;
+        return S1D_OK;
+    }
+    const auto& sh = s->impl.shards[static_cast<std::size_t>(s->impl.locals[0])];
+    *start = sh.start;
+    *count = sh.N;
+    return S1D_OK;
+}
 
 int s1d_run(const s1d_config* cfg, double* state_out, size_t state_len, s1d_stats* stats, s1d_timing* timing,
             char* err, size_t errlen) {
@@ -674,7 +884,7 @@ int s1d_run(const s1d_config* cfg, double* state_out, size_t state_len, s1d_stat
         s1d_timing t{};
         solver.advance(stats, &t);
         const auto t2 = std::chrono::steady_clock::now();
-        solver.download(state_out);
+        solver.download(state_out, false);
         t.d2h_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
         if (timing) *timing = t;
     });

@@ -77,10 +77,8 @@ void validate(const s1d_config& cfg, bool partitioned) {
 
 void finalize(s1d_config& cfg, bool partitioned) {
     validate(cfg, partitioned);
-    if (cfg.equation == S1D_EULER && cfg.dt_dx == 0.0) {
-        const auto ic = initial_condition(initial_or_default(cfg), cfg.grid_size, cfg.equation, cfg.gamma);
-        cfg.dt_dx = cfg.cfl / max_signal_speed(ic.data(), ic.size(), cfg.gamma);
-    }
+    if (cfg.equation == S1D_EULER && cfg.dt_dx == 0.0)
+        cfg.dt_dx = cfg.cfl / max_signal_speed_of(initial_or_default(cfg), cfg.grid_size, cfg.gamma);
 }
 
 void apply_config_entry(s1d_config& cfg, const std::string& key, const std::string& value) {
@@ -142,12 +140,13 @@ static double sine_sample(std::uint64_t j, std::uint64_t n) {
     return sign * std::sin(2.0 * M_PI * static_cast<double>(folded) / static_cast<double>(n));
 }
 
-std::vector<double> initial_condition(const std::string& id, std::uint64_t n, int equation, double gamma) {
+std::vector<double> initial_condition_range(const std::string& id, std::uint64_t n, int equation, double gamma,
+                                            std::uint64_t j0, std::uint64_t count) {
     std::vector<double> out;
     if (equation == S1D_HEAT) {
-        out.resize(n);
+        out.resize(count);
         if (id == "heat-sine") {
-            for (std::uint64_t j = 0; j < n; ++j) out[j] = sine_sample(j, n);
+            for (std::uint64_t j = 0; j < count; ++j) out[j] = sine_sample(j0 + j, n);
         } else if (id == "uniform") {
             std::fill(out.begin(), out.end(), 1.0);
         } else {
@@ -157,15 +156,31 @@ std::vector<double> initial_condition(const std::string& id, std::uint64_t n, in
     }
     const bool sod = id == "euler-sod-periodic";
     if (!sod && id != "uniform") throw Error(S1D_UNKNOWN_IC, "initial condition '" + id + "' unknown for euler");
-    out.resize(3 * n);
-    for (std::uint64_t j = 0; j < n; ++j) {
+    out.resize(3 * count);
+    for (std::uint64_t i = 0; i < count; ++i) {
+        const std::uint64_t j = j0 + i;
         const bool right = sod && !(2 * j < n);
         const double rho = right ? 0.125 : 1.0, u = 0.0, p = right ? 0.1 : 1.0;
-        out[3 * j] = rho;
-        out[3 * j + 1] = rho * u;
-        out[3 * j + 2] = p / (gamma - 1.0) + 0.5 * rho * u * u;
+        out[3 * i] = rho;
+        out[3 * i + 1] = rho * u;
+        out[3 * i + 2] = p / (gamma - 1.0) + 0.5 * rho * u * u;
     }
     return out;
+}
+
+std::vector<double> initial_condition(const std::string& id, std::uint64_t n, int equation, double gamma) {
+    return initial_condition_range(id, n, equation, gamma, 0, n);
+}
+
+double max_signal_speed_of(const std::string& id, std::uint64_t n, double gamma) {
+    double best = 0.0;
+    const std::uint64_t chunk = 1 << 20;
+    for (std::uint64_t j0 = 0; j0 < n; j0 += chunk) {
+        const std::uint64_t c = std::min(chunk, n - j0);
+        const auto v = initial_condition_range(id, n, S1D_EULER, gamma, j0, c);
+        best = std::max(best, max_signal_speed(v.data(), v.size(), gamma));
+    }
+    return best;
 }
 
 static double host_pressure(double rho, double mom, double ene, double gamma) {

@@ -37,7 +37,13 @@ void finalize(s1d_config& cfg, bool partitioned);
 void apply_config_entry(s1d_config& cfg, const std::string& key, const std::string& value);
 
 std::vector<double> initial_condition(const std::string& id, std::uint64_t n, int equation, double gamma);
+// Points [j0, j0+count) of the same initial condition (vpp doubles each):
+// per-point identical to initial_condition(), without materialising all n.
+std::vector<double> initial_condition_range(const std::string& id, std::uint64_t n, int equation, double gamma,
+                                            std::uint64_t j0, std::uint64_t count);
 double max_signal_speed(const double* prim, std::size_t len, double gamma);
+// max_signal_speed over the whole initial condition, streamed in chunks.
+double max_signal_speed_of(const std::string& id, std::uint64_t n, double gamma);
 
 struct Partition {
     std::vector<std::uint64_t> blocks, start;

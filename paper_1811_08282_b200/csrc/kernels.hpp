@@ -69,4 +69,9 @@ cudaError_t launch_euler_pack(const double* st_fields, double* aos, std::uint64_
                               cudaStream_t st);
 std::size_t euler_tile_smem_bytes(int flat, int w);
 
+// one-process-per-GPU round ordering (sync.cu)
+cudaError_t launch_wait_flags(const unsigned* flags, unsigned seq, int* err, std::uint64_t timeout_ns,
+                              cudaStream_t st);
+cudaError_t launch_signal_flags(unsigned* left_slot, unsigned* right_slot, unsigned seq, cudaStream_t st);
+
 } // namespace s1d
