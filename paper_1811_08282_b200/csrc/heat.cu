@@ -156,6 +156,161 @@ __device__ __forceinline__ void insert_level(const TileCtx<P>& c, double (&v)[P]
     }
 }
 
+// ---------------------------------------------------------------------------
+// Level loops in segments. Over a phase each warp's role changes only at a
+// handful of levels (the span edges sweep across it once), so the levels are
+// run in segments with compile-time role flags: an idle warp costs a barrier
+// per level, a computing warp publish + barrier + 5P FP64 ops.
+// ---------------------------------------------------------------------------
+template <int P>
+__device__ __forceinline__ void compute_span(const TileCtx<P>& c, double (&v)[P], int r, double fo) {
+    const int par = (r & 1) * c.xs;
+    const double lft = c.XL[par + c.slot - 1];
+    const double rgt = c.XF[par + c.slot + 1];
+    double nv[P];
+    if (P == 1) {
+        nv[0] = heat_f(lft, v[0], rgt, fo);
+    } else {
+        nv[0] = heat_f(lft, v[0], v[1], fo);
+#pragma unroll
+        for (int k = 1; k < P - 1; ++k) nv[k] = heat_f(v[k - 1], v[k], v[k + 1], fo);
+        nv[P - 1] = heat_f(v[P - 2], v[P - 1], rgt, fo);
+    }
+#pragma unroll
+    for (int k = 0; k < P; ++k) v[k] = nv[k];
+}
+
+template <int P>
+__device__ __forceinline__ void insert_left(const TileCtx<P>& c, double (&v)[P], int r, int lo) {
+    const int base = 2 * (r - 1) - (lo - 1) + c.my_lo;
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (c.my_lo + k <= lo) v[k] = c.einR[(base + k) & kRingMask];
+}
+template <int P>
+__device__ __forceinline__ void insert_right(const TileCtx<P>& c, double (&v)[P], int r, int hi) {
+    const int base = 2 * (r - 1) - (hi - 1) + c.my_lo;
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (c.my_lo + k >= hi - 1) v[k] = c.einL[(base + k) & kRingMask];
+}
+// (`live` only predicates the stores: control flow must stay warp-uniform
+// because the segment loops contain barriers.)
+template <int P>
+__device__ __forceinline__ void export_left(const TileCtx<P>& c, const double (&v)[P], int d, int lo, double* oL,
+                                            bool live) {
+    double* dst = oL + 2 * d - lo + c.my_lo;
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (live && (unsigned)(c.my_lo + k - lo) < 2u) dst[k] = v[k];
+}
+template <int P>
+__device__ __forceinline__ void export_right(const TileCtx<P>& c, const double (&v)[P], int d, int hi, double* oR,
+                                             bool live) {
+    double* dst = oR + 2 * d - (hi - 2) + c.my_lo;
+#pragma unroll
+    for (int k = 0; k < P; ++k)
+        if (live && (unsigned)(c.my_lo + k - (hi - 2)) < 2u) dst[k] = v[k];
+}
+
+// Expanding levels [r0, r1): span [w/2+1-r, w/2+1+r).
+template <int P, bool IL, bool IR, bool CP, class Feed>
+__device__ __forceinline__ void expand_seg(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
+                                           Feed& feed) {
+    for (int r = r0; r < r1; ++r) {
+        const int lo = c.w / 2 + 1 - r, hi = c.w / 2 + 1 + r;
+        if (IL) insert_left(c, v, r, lo);
+        if (IR) insert_right(c, v, r, hi);
+        if (IL || IR || CP) publish(c, v, r);
+        feed(r);
+        __syncthreads();
+        if (CP) compute_span(c, v, r, fo);
+    }
+}
+
+template <int P, class Feed>
+__device__ __forceinline__ void expand_levels(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
+                                              Feed& feed) {
+    const int h2 = c.w / 2;
+    // role ranges (inclusive) for this warp's x in [wlo, whi]
+    const int rc = max(h2 + 1 - c.whi, c.wlo - h2);  // computes from rc on
+    const int aL = h2 - c.whi, bL = h2 + 1 - c.wlo;  // left inserts
+    const int aR = c.wlo - h2 - 1, bR = c.whi - h2;  // right inserts
+    int bnd[6] = {rc, aL, bL + 1, aR, bR + 1, r1};
+#pragma unroll
+    for (int i = 1; i < 6; ++i) // insertion sort (6 warp-uniform ints)
+        for (int j = i; j > 0 && bnd[j - 1] > bnd[j]; --j) {
+            const int tmp = bnd[j];
+            bnd[j] = bnd[j - 1];
+            bnd[j - 1] = tmp;
+        }
+    int r = r0;
+#pragma unroll 1
+    for (int i = 0; i < 6 && r < r1; ++i) {
+        const int e = min(max(bnd[i], r), r1);
+        if (e <= r) continue;
+        const int f = ((r >= aL && r <= bL) ? 4 : 0) | ((r >= aR && r <= bR) ? 2 : 0) | (r >= rc ? 1 : 0);
+        switch (f) {
+        case 0: expand_seg<P, false, false, false>(c, v, r, e, fo, feed); break;
+        case 1: expand_seg<P, false, false, true>(c, v, r, e, fo, feed); break;
+        case 2: expand_seg<P, false, true, false>(c, v, r, e, fo, feed); break;
+        case 3: expand_seg<P, false, true, true>(c, v, r, e, fo, feed); break;
+        case 4: expand_seg<P, true, false, false>(c, v, r, e, fo, feed); break;
+        case 5: expand_seg<P, true, false, true>(c, v, r, e, fo, feed); break;
+        case 6: expand_seg<P, true, true, false>(c, v, r, e, fo, feed); break;
+        default: expand_seg<P, true, true, true>(c, v, r, e, fo, feed); break;
+        }
+        r = e;
+    }
+}
+
+// Contracting levels [r0, r1): d = r-m, span [1+d, 1+w-d).
+template <int P, bool PB, bool CP, bool EL, bool ER>
+__device__ __forceinline__ void contract_seg(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
+                                             double* oL, double* oR, bool live) {
+    for (int r = r0; r < r1; ++r) {
+        const int d = r - c.m, lo = 1 + d, hi = 1 + c.w - d;
+        if (PB) publish(c, v, r);
+        __syncthreads();
+        if (CP) compute_span(c, v, r, fo);
+        if (EL) export_left(c, v, d, lo, oL, live);
+        if (ER) export_right(c, v, d, hi, oR, live);
+    }
+}
+
+template <int P>
+__device__ __forceinline__ void contract_levels(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
+                                                double* oL, double* oR, bool live) {
+    const int m = c.m, w = c.w;
+    const int rce = m + min(c.whi - 1, w - c.wlo);      // computes while r <= rce
+    const int rpe = m + min(c.whi, w + 1 - c.wlo);      // publishes while r <= rpe
+    const int aL = m + c.wlo - 2, bL = m + c.whi - 1;   // left exports
+    const int aR = m + w - 1 - c.whi, bR = m + w - c.wlo; // right exports
+    int bnd[7] = {rce + 1, rpe + 1, aL, bL + 1, aR, bR + 1, r1};
+#pragma unroll
+    for (int i = 1; i < 7; ++i)
+        for (int j = i; j > 0 && bnd[j - 1] > bnd[j]; --j) {
+            const int tmp = bnd[j];
+            bnd[j] = bnd[j - 1];
+            bnd[j - 1] = tmp;
+        }
+    int r = r0;
+#pragma unroll 1
+    for (int i = 0; i < 7 && r < r1; ++i) {
+        const int e = min(max(bnd[i], r), r1);
+        if (e <= r) continue;
+        const bool pb = r <= rpe, cp = r <= rce;
+        const bool el = r >= aL && r <= bL, er = r >= aR && r <= bR; // warp-uniform
+        if (!pb) contract_seg<P, false, false, false, false>(c, v, r, e, fo, oL, oR, live);
+        else if (!cp) contract_seg<P, true, false, false, false>(c, v, r, e, fo, oL, oR, live);
+        else if (el && er) contract_seg<P, true, true, true, true>(c, v, r, e, fo, oL, oR, live);
+        else if (el) contract_seg<P, true, true, true, false>(c, v, r, e, fo, oL, oR, live);
+        else if (er) contract_seg<P, true, true, false, true>(c, v, r, e, fo, oL, oR, live);
+        else contract_seg<P, true, true, false, false>(c, v, r, e, fo, oL, oR, live);
+        r = e;
+    }
+}
+
 template <int P, int KIND, int MAXT>
 __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ double sm[];
@@ -240,15 +395,8 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
     double* oR = a.out_R + (std::size_t)b * w;
 
     if (KIND != kUp) {
-        // Expanding half, levels 1..m: span [w/2+1-r, w/2+1+r).
-        for (int r = 1; r < m; ++r) {
-            const int lo = w / 2 + 1 - r, hi = w / 2 + 1 + r;
-            insert_level(c, v, r, lo, hi);
-            publish(c, v, r);
-            feed(r);
-            __syncthreads();
-            compute_level(c, v, r, lo, hi, fo);
-        }
+        // Expanding half, levels 1..m-1 (span [w/2+1-r, w/2+1+r)), then m.
+        expand_levels(c, v, 1, m, fo, feed);
         {
             const int r = m, lo = 1, hi = w + 1;
             insert_level(c, v, r, lo, hi);
@@ -264,13 +412,7 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
     if (KIND != kDown) {
         // Contracting half, levels m..2m-1: span [1+d, 1+w-d), d = r-m.
         if (live) export_level(c, v, 0, 1, w + 1, oL, oR);
-        for (int r = m + 1; r <= 2 * m - 1; ++r) {
-            const int d = r - m, lo = 1 + d, hi = 1 + w - d;
-            publish(c, v, r);
-            __syncthreads();
-            compute_level(c, v, r, lo, hi, fo);
-            if (live) export_level(c, v, d, lo, hi, oL, oR);
-        }
+        contract_levels(c, v, m + 1, 2 * m, fo, oL, oR, live);
     } else if (live) {
         const std::int64_t g0 = centre - w / 2 + (std::int64_t)c.lt * P;
 #pragma unroll
