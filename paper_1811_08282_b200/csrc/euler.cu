@@ -175,61 +175,75 @@ struct TileGeom {
     static constexpr int CHUNKS = LVL / 2;    // 16-byte chunks per level per side
 };
 
-inline std::size_t euler_tile_smem(int flat, int w) {
+// Shared memory of one tile (doubles): records, pressures, fluxes, ring.
+inline std::size_t euler_tile_doubles(int flat, int w) {
     const int H = flat ? 2 : 1, REC = flat ? 6 : 7;
     const std::size_t W2 = (std::size_t)w + 2 * H;
-    const std::size_t s = REC * W2 + (W2 + 1) + 3 * (W2 + 1) + 2 * (std::size_t)kERing * 2 * H * REC;
-    return s * sizeof(double);
+    return REC * W2 + (W2 + 1) + 3 * (W2 + 1) + 2 * (std::size_t)kERing * 2 * H * REC;
+}
+inline std::size_t euler_tile_smem(int flat, int w) { return euler_tile_doubles(flat, w) * sizeof(double); }
+
+// Narrow tiles share a CTA (GT tiles side by side) so each phase has enough
+// points for the CTA's threads.
+inline int euler_tiles_per_cta(int flat, int w) {
+    const int H = flat ? 2 : 1, chunks = flat ? 12 : 7; // 16-byte edge chunks per level and side
+    int gt = 1;
+    while (gt < 16 && (std::size_t)(2 * gt) * (w + 2 * H) <= 512 &&
+           (std::size_t)(2 * gt) * euler_tile_smem(flat, w) <= 100 * 1024 && 2 * chunks * (2 * gt) <= 256)
+        gt *= 2;
+    if (const char* e = std::getenv("S1D_EULER_GT")) {
+        const int v = std::atoi(e);
+        if (v >= 1 && v <= 64 && 2 * chunks * v <= 256) gt = v;
+    }
+    return gt;
 }
 
 template <int FLAT, int KIND>
-__global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs a) {
+__global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs a, int GT) {
     using G = TileGeom<FLAT>;
     constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
     extern __shared__ double sm[];
-    const int w = a.w, m = a.m, b = blockIdx.x, t = threadIdx.x, NT = blockDim.x;
+    const int w = a.w, m = a.m, t = threadIdx.x, NT = blockDim.x;
     const int W2 = w + 2 * H;
-    double* S = sm;                      // [REC][W2] records, local x in [0, W2)
-    double* P = S + REC * W2;            // [W2+1] pressures
-    double* Fx = P + (W2 + 1);           // [3][W2+1] interface fluxes (interface x: between x-1 and x)
-    double* ring = Fx + 3 * (W2 + 1);    // [2 sides][kERing][LVL]
+    const std::size_t TS = (std::size_t)REC * W2 + 4 * (std::size_t)(W2 + 1) + 2 * (std::size_t)kERing * LVL;
+    // per-tile views: S [REC][W2] records (local x in [0, W2)), P [W2+1]
+    // pressures, Fx [3][W2+1] interface fluxes (interface x between x-1 and
+    // x), ring [2 sides][kERing][LVL]
+    auto S = [&](int gi) { return sm + gi * TS; };
+    auto Pp = [&](int gi) { return sm + gi * TS + REC * W2; };
+    auto Fx = [&](int gi) { return sm + gi * TS + REC * W2 + (W2 + 1); };
+    auto ring = [&](int gi) { return sm + gi * TS + REC * W2 + 4 * (W2 + 1); };
     const double gamma = a.gamma;
     const double dt_dx = a.dt_dx;
+    const std::size_t tstride = (std::size_t)w * REC; // edge doubles per tile per side
     bool bad = false;
 
-    const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
-    const std::int64_t g0 = centre - w / 2 - H; // shard position of local x = 0
-
-    // producers' edges (Diamond/Down)
-    const double* pR = nullptr;
-    const double* pL = nullptr;
-    const std::size_t tstride = (std::size_t)w * REC; // edge doubles per tile per side
-    // feeders: threads [0, CHUNKS) copy the left (R-edge) chunks, [CHUNKS, 2*CHUNKS) the right
-    const bool feeder = KIND != kUp && t < 2 * G::CHUNKS;
-    const int fside = t < G::CHUNKS ? 0 : 1, fchunk = t % G::CHUNKS;
-    auto issue = [&](int q) { // level q (1-based) into its ring slot
-        if (feeder && q <= m) {
-            const double* src = (fside == 0 ? pR : pL) + (std::size_t)(q - 1) * LVL + 2 * fchunk;
-            double* dst = ring + ((std::size_t)fside * kERing + (q - 1) % kERing) * LVL + 2 * fchunk;
-            cp_async16(dst, src);
-        }
+    auto tile_of = [&](int gi) { return (int)blockIdx.x * GT + gi; };
+    auto live = [&](int gi) { return tile_of(gi) < a.nb; };
+    auto origin = [&](int gi) { // shard position of local x = 0
+        const int b = tile_of(gi);
+        const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
+        return centre - w / 2 - H;
     };
-    // copy level q's ring slot into S: left records at x in [lo-H, lo+H),
-    // right at [hi-H, hi+H) with lo/hi the span of level q.
-    auto insert = [&](int q) {
-        const int lo = w / 2 + H - q * H, hi = w / 2 + H + q * H;
-        for (int i = t; i < 2 * LVL; i += NT) {
-            const int side = i / LVL, j = i % LVL, rec = j / REC, f = j % REC;
-            const int x = side == 0 ? lo - H + rec : hi - H + rec;
-            S[f * W2 + x] = ring[((std::size_t)side * kERing + (q - 1) % kERing) * LVL + j];
+    // Visit (tile, x) for x in [x0, x1) of every live tile, threads spread
+    // over the concatenation of the tiles' ranges.
+    auto for_all = [&](int x0, int x1, auto&& f) {
+        const int cnt = x1 - x0;
+        if (cnt <= 0) return;
+        if (GT == 1) {
+            if (live(0))
+                for (int x = x0 + t; x < x1; x += NT) f(0, x);
+            return;
+        }
+        for (int i = t; i < GT * cnt; i += NT) {
+            const int gi = i / cnt;
+            if (live(gi)) f(gi, x0 + (i - gi * cnt));
         }
     };
 
-    if (KIND == kUp) {
-        for (int f = 0; f < REC; ++f)
-            for (int x = H + t; x < w + H; x += NT)
-                S[f * W2 + x] = a.state_in[(std::size_t)f * a.fstride + (std::size_t)(g0 + x)];
-    } else {
+    // producers' edges (Diamond/Down); feeders: per tile, CHUNKS threads per side
+    auto producers = [&](int gi, const double*& pR, const double*& pL) {
+        const int b = tile_of(gi);
         if (a.seam) {
             pR = a.in_R + (std::size_t)b * tstride;
             pL = (b + 1 < a.nb) ? a.in_L + (std::size_t)(b + 1) * tstride : a.peer_L;
@@ -237,6 +251,44 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
             pR = (b > 0) ? a.in_R + (std::size_t)(b - 1) * tstride : a.peer_R;
             pL = a.in_L + (std::size_t)b * tstride;
         }
+    };
+    const int fg = t / (2 * G::CHUNKS);
+    const bool feeder = KIND != kUp && fg < GT && live(fg);
+    const int fside = (t % (2 * G::CHUNKS)) < G::CHUNKS ? 0 : 1, fchunk = t % G::CHUNKS;
+    const double* fsrc = nullptr;
+    double* fring = nullptr;
+    if (feeder) {
+        const double* pR;
+        const double* pL;
+        producers(fg, pR, pL);
+        fsrc = (fside == 0 ? pR : pL) + 2 * fchunk;
+        fring = ring(fg) + (std::size_t)fside * kERing * LVL + 2 * fchunk;
+    }
+    auto issue = [&](int q) { // level q (1-based) into its ring slot
+        if (feeder && q <= m) cp_async16(fring + (std::size_t)((q - 1) % kERing) * LVL, fsrc + (std::size_t)(q - 1) * LVL);
+    };
+    // copy level q's ring slot into S: left records at x in [lo-H, lo+H),
+    // right at [hi-H, hi+H) with lo/hi the span of level q.
+    auto insert = [&](int q) {
+        const int lo = w / 2 + H - q * H, hi = w / 2 + H + q * H;
+        for (int i = t; i < GT * 2 * LVL; i += NT) {
+            const int gi = i / (2 * LVL), k = i % (2 * LVL);
+            if (!live(gi)) continue;
+            const int side = k / LVL, j = k % LVL, rec = j / REC, f = j % REC;
+            const int x = side == 0 ? lo - H + rec : hi - H + rec;
+            S(gi)[f * W2 + x] = ring(gi)[((std::size_t)side * kERing + (q - 1) % kERing) * LVL + j];
+        }
+    };
+
+    if (KIND == kUp) {
+        for (int gi = 0; gi < GT; ++gi) {
+            if (!live(gi)) continue;
+            const std::int64_t g0 = origin(gi);
+            for (int f = 0; f < REC; ++f)
+                for (int x = H + t; x < w + H; x += NT)
+                    S(gi)[f * W2 + x] = a.state_in[(std::size_t)f * a.fstride + (std::size_t)(g0 + x)];
+        }
+    } else {
         for (int q = 1; q <= kELook; ++q) {
             issue(q);
             if (feeder) cp_async_commit();
@@ -254,72 +306,90 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
         if (!FLAT) {
             if (c & 1) {
                 const int s = ((c & 3) == 1) ? 0 : 3;
-                for (int x = lo - 1 + t; x < hi + 1; x += NT)
-                    P[x] = em::pressure(S[s * W2 + x], S[(s + 1) * W2 + x], S[(s + 2) * W2 + x], gamma, bad);
+                for_all(lo - 1, hi + 1, [&](int gi, int x) {
+                    const double* St = S(gi);
+                    Pp(gi)[x] = em::pressure(St[s * W2 + x], St[(s + 1) * W2 + x], St[(s + 2) * W2 + x], gamma, bad);
+                });
                 between(0);
                 __syncthreads();
-                for (int x = lo + t; x < hi; x += NT) S[6 * W2 + x] = em::ratio(P[x - 1], P[x], P[x + 1]);
+                for_all(lo, hi, [&](int gi, int x) {
+                    const double* P = Pp(gi);
+                    S(gi)[6 * W2 + x] = em::ratio(P[x - 1], P[x], P[x + 1]);
+                });
                 between(1);
             } else {
                 const bool fin = (c & 3) == 0;
                 const int rs = fin ? 3 : 0, ws = fin ? 0 : 3;
                 const double factor = fin ? dt_dx : em::mul(0.5, dt_dx);
-                for (int x = lo + t; x < hi + 1; x += NT) {
+                for_all(lo, hi + 1, [&](int gi, int x) {
+                    const double* St = S(gi);
+                    double* F = Fx(gi);
                     double f0, f1, f2;
-                    em::iflux(S[rs * W2 + x - 1], S[(rs + 1) * W2 + x - 1], S[(rs + 2) * W2 + x - 1], S[rs * W2 + x],
-                              S[(rs + 1) * W2 + x], S[(rs + 2) * W2 + x], S[6 * W2 + x - 1], S[6 * W2 + x], gamma, f0,
-                              f1, f2, bad);
-                    Fx[x] = f0;
-                    Fx[(W2 + 1) + x] = f1;
-                    Fx[2 * (W2 + 1) + x] = f2;
-                }
+                    em::iflux(St[rs * W2 + x - 1], St[(rs + 1) * W2 + x - 1], St[(rs + 2) * W2 + x - 1], St[rs * W2 + x],
+                              St[(rs + 1) * W2 + x], St[(rs + 2) * W2 + x], St[6 * W2 + x - 1], St[6 * W2 + x], gamma,
+                              f0, f1, f2, bad);
+                    F[x] = f0;
+                    F[(W2 + 1) + x] = f1;
+                    F[2 * (W2 + 1) + x] = f2;
+                });
                 between(0);
                 __syncthreads();
-                for (int x = lo + t; x < hi; x += NT) {
+                for_all(lo, hi, [&](int gi, int x) {
+                    double* St = S(gi);
+                    const double* F = Fx(gi);
 #pragma unroll
                     for (int k = 0; k < 3; ++k)
-                        S[(ws + k) * W2 + x] =
-                            em::update(S[k * W2 + x], factor, Fx[k * (W2 + 1) + x + 1], Fx[k * (W2 + 1) + x]);
-                }
+                        St[(ws + k) * W2 + x] =
+                            em::update(St[k * W2 + x], factor, F[k * (W2 + 1) + x + 1], F[k * (W2 + 1) + x]);
+                });
                 between(1);
             }
         } else {
             const bool fin = (c & 1) == 0;
             const int s = fin ? 3 : 0, ws = fin ? 0 : 3;
             const double factor = fin ? dt_dx : em::mul(0.5, dt_dx);
-            for (int x = lo - 2 + t; x < hi + 2; x += NT)
-                P[x] = em::pressure(S[s * W2 + x], S[(s + 1) * W2 + x], S[(s + 2) * W2 + x], gamma, bad);
+            for_all(lo - 2, hi + 2, [&](int gi, int x) {
+                const double* St = S(gi);
+                Pp(gi)[x] = em::pressure(St[s * W2 + x], St[(s + 1) * W2 + x], St[(s + 2) * W2 + x], gamma, bad);
+            });
             __syncthreads();
-            for (int x = lo + t; x < hi + 1; x += NT) {
+            for_all(lo, hi + 1, [&](int gi, int x) {
+                const double* St = S(gi);
+                const double* P = Pp(gi);
+                double* F = Fx(gi);
                 const double rl = em::ratio(P[x - 2], P[x - 1], P[x]);
                 const double rr = em::ratio(P[x - 1], P[x], P[x + 1]);
                 double f0, f1, f2;
-                em::iflux(S[s * W2 + x - 1], S[(s + 1) * W2 + x - 1], S[(s + 2) * W2 + x - 1], S[s * W2 + x],
-                          S[(s + 1) * W2 + x], S[(s + 2) * W2 + x], rl, rr, gamma, f0, f1, f2, bad);
-                Fx[x] = f0;
-                Fx[(W2 + 1) + x] = f1;
-                Fx[2 * (W2 + 1) + x] = f2;
-            }
+                em::iflux(St[s * W2 + x - 1], St[(s + 1) * W2 + x - 1], St[(s + 2) * W2 + x - 1], St[s * W2 + x],
+                          St[(s + 1) * W2 + x], St[(s + 2) * W2 + x], rl, rr, gamma, f0, f1, f2, bad);
+                F[x] = f0;
+                F[(W2 + 1) + x] = f1;
+                F[2 * (W2 + 1) + x] = f2;
+            });
             between(0);
             __syncthreads();
-            for (int x = lo + t; x < hi; x += NT) {
+            for_all(lo, hi, [&](int gi, int x) {
+                double* St = S(gi);
+                const double* F = Fx(gi);
 #pragma unroll
                 for (int k = 0; k < 3; ++k)
-                    S[(ws + k) * W2 + x] =
-                        em::update(S[k * W2 + x], factor, Fx[k * (W2 + 1) + x + 1], Fx[k * (W2 + 1) + x]);
-            }
+                    St[(ws + k) * W2 + x] =
+                        em::update(St[k * W2 + x], factor, F[k * (W2 + 1) + x + 1], F[k * (W2 + 1) + x]);
+            });
             between(1);
         }
         __syncthreads();
     };
 
     auto export_level = [&](int d, int lo, int hi) {
-        double* oL = a.out_L + (std::size_t)b * tstride + (std::size_t)d * LVL;
-        double* oR = a.out_R + (std::size_t)b * tstride + (std::size_t)d * LVL;
-        for (int i = t; i < 2 * LVL; i += NT) {
-            const int side = i / LVL, j = i % LVL, rec = j / REC, f = j % REC;
+        for (int i = t; i < GT * 2 * LVL; i += NT) {
+            const int gi = i / (2 * LVL), k = i % (2 * LVL);
+            if (!live(gi)) continue;
+            const int b = tile_of(gi);
+            const int side = k / LVL, j = k % LVL, rec = j / REC, f = j % REC;
             const int x = side == 0 ? lo + rec : hi - 2 * H + rec;
-            (side == 0 ? oL : oR)[j] = S[f * W2 + x];
+            double* o = (side == 0 ? a.out_L : a.out_R) + (std::size_t)b * tstride + (std::size_t)d * LVL;
+            o[j] = S(gi)[f * W2 + x];
         }
     };
 
@@ -348,34 +418,41 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
             export_level(d, lo, hi);
         }
     } else {
-        for (int f = 0; f < REC; ++f)
-            for (int x = H + t; x < w + H; x += NT) {
-                const std::uint64_t gp = (std::uint64_t)(g0 + x);
-                if (gp < a.N) a.state_out[(std::size_t)f * a.fstride + gp] = S[f * W2 + x];
-                else a.state_right[(std::size_t)f * a.right_fstride + (gp - a.N)] = S[f * W2 + x];
-            }
+        for (int gi = 0; gi < GT; ++gi) {
+            if (!live(gi)) continue;
+            const std::int64_t g0 = origin(gi);
+            for (int f = 0; f < REC; ++f)
+                for (int x = H + t; x < w + H; x += NT) {
+                    const std::uint64_t gp = (std::uint64_t)(g0 + x);
+                    if (gp < a.N) a.state_out[(std::size_t)f * a.fstride + gp] = S(gi)[f * W2 + x];
+                    else a.state_right[(std::size_t)f * a.right_fstride + (gp - a.N)] = S(gi)[f * W2 + x];
+                }
+        }
     }
     raise_flag(a.error_flag, bad);
 }
 
 template <int FLAT>
 cudaError_t launch_tile_f(int kind, const TileArgs& a, cudaStream_t st) {
-    const size_t smem = euler_tile_smem(FLAT, a.w);
-    void (*k)(const TileArgs) = kind == kUp ? euler_tile<FLAT, kUp>
-                                : kind == kDiamond ? euler_tile<FLAT, kDiamond>
-                                                   : euler_tile<FLAT, kDown>;
+    const int GT = euler_tiles_per_cta(FLAT, a.w);
+    const size_t smem = (size_t)GT * euler_tile_smem(FLAT, a.w);
+    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp>
+                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond>
+                                                        : euler_tile<FLAT, kDown>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     // narrow tiles: 128-thread CTAs (more tiles in flight per SM)
-    int cap = a.w <= 256 ? 128 : 256;
+    int cap = a.w <= 256 && GT == 1 ? 128 : 256;
     if (const char* e = std::getenv("S1D_EULER_NT")) cap = std::atoi(e);
     if (cap < 32 || cap > 256) cap = 256;
-    int nt = ((a.w + 2 * TileGeom<FLAT>::H + 31) / 32) * 32;
+    int nt = ((GT * (a.w + 2 * TileGeom<FLAT>::H) + 31) / 32) * 32;
     if (nt > cap) nt = cap;
-    if (nt < 2 * TileGeom<FLAT>::CHUNKS) nt = 32 * ((2 * TileGeom<FLAT>::CHUNKS + 31) / 32);
-    k<<<a.nb, nt, smem, st>>>(a);
+    const int need = 32 * ((2 * TileGeom<FLAT>::CHUNKS * GT + 31) / 32); // feeder threads
+    if (nt < need) nt = need;
+    const unsigned grid = (unsigned)((a.nb + GT - 1) / GT);
+    k<<<grid, nt, smem, st>>>(a, GT);
     return cudaGetLastError();
 }
 
