@@ -187,10 +187,14 @@ inline std::size_t euler_tile_smem(int flat, int w) { return euler_tile_doubles(
 // points for the CTA's threads.
 inline int euler_tiles_per_cta(int flat, int w) {
     const int H = flat ? 2 : 1, chunks = flat ? 12 : 7; // 16-byte edge chunks per level and side
+    // measured (B200, n=2^22): lengthening best at GT*w ~ 512 for w <= 128;
+    // flattening at GT = 8, 4, 4 for w = 32, 64, 128; wide tiles alone.
     int gt = 1;
-    while (gt < 16 && (std::size_t)(2 * gt) * (w + 2 * H) <= 512 &&
-           (std::size_t)(2 * gt) * euler_tile_smem(flat, w) <= 100 * 1024 && 2 * chunks * (2 * gt) <= 256)
+    const int want = w > 128 ? 1 : flat ? (w <= 32 ? 8 : 4) : 512 / w;
+    while (gt < want && gt < 16 && (std::size_t)(2 * gt) * euler_tile_smem(flat, w) <= 100 * 1024 &&
+           2 * chunks * (2 * gt) <= 256)
         gt *= 2;
+    (void)H;
     if (const char* e = std::getenv("S1D_EULER_GT")) {
         const int v = std::atoi(e);
         if (v >= 1 && v <= 64 && 2 * chunks * v <= 256) gt = v;

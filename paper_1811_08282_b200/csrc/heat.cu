@@ -156,6 +156,14 @@ __device__ __forceinline__ void insert_level(const TileCtx<P>& c, double (&v)[P]
     }
 }
 
+// Diagnostic builds (-DS1D_NO_LEVEL_BARRIER) replace the level barrier with
+// __syncwarp() to time the level loop without it (results are then wrong).
+#ifdef S1D_NO_LEVEL_BARRIER
+#define S1D_LEVEL_BARRIER() __syncwarp()
+#else
+#define S1D_LEVEL_BARRIER() __syncthreads()
+#endif
+
 // ---------------------------------------------------------------------------
 // Level loops in segments. Over a phase each warp's role changes only at a
 // handful of levels (the span edges sweep across it once), so the levels are
@@ -223,7 +231,7 @@ __device__ __forceinline__ void expand_seg(const TileCtx<P>& c, double (&v)[P], 
         if (IR) insert_right(c, v, r, hi);
         if (IL || IR || CP) publish(c, v, r);
         feed(r);
-        __syncthreads();
+        S1D_LEVEL_BARRIER();
         if (CP) compute_span(c, v, r, fo);
     }
 }
@@ -271,7 +279,7 @@ __device__ __forceinline__ void contract_seg(const TileCtx<P>& c, double (&v)[P]
     for (int r = r0; r < r1; ++r) {
         const int d = r - c.m, lo = 1 + d, hi = 1 + c.w - d;
         if (PB) publish(c, v, r);
-        __syncthreads();
+        S1D_LEVEL_BARRIER();
         if (CP) compute_span(c, v, r, fo);
         if (EL) export_left(c, v, d, lo, oL, live);
         if (ER) export_right(c, v, d, hi, oR, live);
