@@ -192,6 +192,37 @@ int s1d_shard_export(s1d_solver* s, void* blob, size_t blob_len);
 int s1d_shard_connect(s1d_solver* s, const void* left_blob, const void* right_blob);
 int s1d_shard_range(const s1d_solver* s, uint64_t* start, uint64_t* count);
 
+/* ---- measurement records, CSV, fits (inc/perf.hpp, inc/csv.hpp) --------- */
+/* TimingRecord (inc/perf.hpp:16-29). avg_us_per_step = loop time / steps
+ * (CUDA events; the reference's WallClock branch of make_record). */
+typedef struct s1d_record {
+    int equation, method, scheme, mode;
+    uint64_t grid_size, block_width;
+    int work_factor, ranks;
+    int64_t steps;
+    double avg_us_per_step;
+    double setup_us;
+    uint64_t messages_sent, bytes_sent, exchange_rounds;
+    double virtual_comm_us; /* always 0 on the B200 path */
+} s1d_record;
+/* measure (src/perf.cpp:29-32): one run of cfg, reduced to a record. */
+int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen);
+/* The reference's fixed 15-column header (inc/csv.hpp:11-13). [host] */
+const char* s1d_csv_header(void);
+/* csv_row (src/csv.cpp:69-78): writes the row (no newline); returns its
+ * length, or -1 if buf is too small. [host] */
+int64_t s1d_csv_row(const s1d_record* r, char* buf, size_t len);
+/* emit_csv (src/csv.cpp:80-99): header + rows in config-lexicographic order. [host] */
+int s1d_emit_csv(const s1d_record* recs, size_t n, const char* path, char* err, size_t errlen);
+/* read_csv (src/csv.cpp:101-136). [host] */
+int s1d_read_csv(const char* path, s1d_record* out, size_t cap, size_t* count, char* err, size_t errlen);
+/* power_law_fit (src/perf.cpp:42-82): y = A x^b by log-log OLS. [host] */
+int s1d_power_law_fit(const double* n, const double* t, size_t count, double* A, double* b, double* r2, char* err,
+                      size_t errlen);
+/* best_config (src/perf.cpp:84-97): index of the fastest record (ties: smaller
+ * w, then smaller WF), or -status. [host] */
+int64_t s1d_best_config(const s1d_record* recs, size_t n);
+
 /* ---- measurement helpers (not part of the reference interface) --------- */
 /* Sustained FP64 DADD/DMUL instruction rate of `device` (ops/s), measured by
  * a dependent-chain-free microkernel: the roofline denominator for the

@@ -21,6 +21,8 @@
 #include <vector>
 
 #include "sweep1d/config.hpp"
+#include "sweep1d/csv.hpp"
+#include "sweep1d/perf.hpp"
 #include "sweep1d/engine.hpp"
 #include "sweep1d/errors.hpp"
 #include "sweep1d/kernels.hpp"
@@ -333,6 +335,72 @@ int ref_model_apply(int model, double* cells, long ncells, long i, long counter,
             }
         }
     });
+}
+
+// ---- post-processing (inc/perf.hpp, inc/csv.hpp) --------------------------
+struct ref_record {
+    int equation, method, scheme, mode;
+    unsigned long long grid_size, block_width;
+    int work_factor, ranks;
+    long long steps;
+    double avg_us_per_step, setup_us;
+    unsigned long long messages_sent, bytes_sent, exchange_rounds;
+    double virtual_comm_us;
+};
+
+static TimingRecord to_rec(const ref_record& r) {
+    TimingRecord t;
+    t.equation = r.equation ? Equation::Euler : Equation::Heat;
+    t.method = r.method ? Method::Flattening : Method::Lengthening;
+    t.scheme = r.scheme ? Scheme::Swept : Scheme::Classic;
+    t.mode = r.mode ? Mode::VirtualTime : Mode::WallClock;
+    t.grid_size = r.grid_size;
+    t.block_width = r.block_width;
+    t.work_factor = r.work_factor;
+    t.ranks = r.ranks;
+    t.steps = static_cast<long>(r.steps);
+    t.avg_us_per_step = r.avg_us_per_step;
+    t.setup_us = r.setup_us;
+    t.stats.messages_sent = r.messages_sent;
+    t.stats.bytes_sent = r.bytes_sent;
+    t.stats.exchange_rounds = r.exchange_rounds;
+    t.stats.virtual_comm_time = r.virtual_comm_us / 1e6;
+    return t;
+}
+
+int ref_csv_row(const ref_record* r, char* buf, size_t len) {
+    const std::string s = csv_row(to_rec(*r));
+    if (s.size() + 1 > len) return -1;
+    std::memcpy(buf, s.c_str(), s.size() + 1);
+    return static_cast<int>(s.size());
+}
+
+int ref_emit_csv(const ref_record* r, size_t n, const char* path, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<TimingRecord> v;
+        for (size_t i = 0; i < n; ++i) v.push_back(to_rec(r[i]));
+        emit_csv(v, std::string(path));
+    });
+}
+
+int ref_power_law_fit(const double* x, const double* y, size_t n, double* A, double* b, double* r2, char* err,
+                      size_t errlen) {
+    return guarded(err, errlen, [&] {
+        std::vector<std::pair<double, double>> pts;
+        for (size_t i = 0; i < n; ++i) pts.emplace_back(x[i], y[i]);
+        const FitResult f = power_law_fit(pts);
+        *A = f.A;
+        *b = f.b;
+        *r2 = f.r_squared;
+    });
+}
+
+long ref_best_config(const ref_record* r, size_t n) {
+    std::vector<TimingRecord> v;
+    for (size_t i = 0; i < n; ++i) v.push_back(to_rec(r[i]));
+    if (v.empty()) return -1;
+    const TimingRecord* b = &best_config(v);
+    return static_cast<long>(b - v.data());
 }
 
 }  // extern "C"

@@ -12,3 +12,6 @@ from .api import (  # noqa: F401
     apply_config_entry, apply_config_file, cycle_advance, device_count, diamond_schedule, down_triangle_schedule,
     initial_condition, initial_condition_range, make_partition, make_spec, max_signal_speed, measure_fp64_peak, run, swept_buffer_cells, to_string,
     triangle_schedule, version, working_array_extents)
+from .api import (  # noqa: F401
+    FitResult, TimingRecord, best_config, csv_header, csv_row, emit_csv, flattening_speedup, measure, power_law_fit,
+    read_csv, speedup)

@@ -39,6 +39,14 @@ class s1d_timing(C.Structure):
                 ("dominant_kernel", C.c_char * 32)]
 
 
+class s1d_record(C.Structure):
+    _fields_ = [("equation", C.c_int), ("method", C.c_int), ("scheme", C.c_int), ("mode", C.c_int),
+                ("grid_size", C.c_uint64), ("block_width", C.c_uint64), ("work_factor", C.c_int),
+                ("ranks", C.c_int), ("steps", C.c_int64), ("avg_us_per_step", C.c_double),
+                ("setup_us", C.c_double), ("messages_sent", C.c_uint64), ("bytes_sent", C.c_uint64),
+                ("exchange_rounds", C.c_uint64), ("virtual_comm_us", C.c_double)]
+
+
 _dp = C.POINTER(C.c_double)
 _E = [C.c_char_p, C.c_size_t]
 
@@ -74,6 +82,13 @@ SIGNATURES = {
                             C.POINTER(s1d_timing)]),
     "s1d_last_error": (C.c_char_p, [C.c_void_p]),
     "s1d_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)] + _E),
+    "s1d_measure": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_record)] + _E),
+    "s1d_csv_header": (C.c_char_p, []),
+    "s1d_csv_row": (C.c_int64, [C.POINTER(s1d_record), C.c_char_p, C.c_size_t]),
+    "s1d_emit_csv": (C.c_int, [C.POINTER(s1d_record), C.c_size_t, C.c_char_p] + _E),
+    "s1d_read_csv": (C.c_int, [C.c_char_p, C.POINTER(s1d_record), C.c_size_t, C.POINTER(C.c_size_t)] + _E),
+    "s1d_power_law_fit": (C.c_int, [_dp, _dp, C.c_size_t, _dp, _dp, _dp] + _E),
+    "s1d_best_config": (C.c_int64, [C.POINTER(s1d_record), C.c_size_t]),
     "s1d_shard_create": (C.c_int, [C.POINTER(s1d_config), C.c_int, C.c_int, C.POINTER(C.c_void_p)] + _E),
     "s1d_shard_blob_size": (C.c_size_t, []),
     "s1d_shard_export": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t]),

@@ -561,3 +561,115 @@ def device_count() -> int:
 
 def version() -> str:
     return lib().s1d_version().decode()
+
+
+# ---------------------------------------------------------------------------
+# measurement records, CSV, fits (inc/perf.hpp, inc/csv.hpp)
+# ---------------------------------------------------------------------------
+@dataclass
+class TimingRecord:
+    """sweep1d::TimingRecord (inc/perf.hpp:16-29)."""
+    equation: Equation = Equation.Heat
+    method: Method = Method.Lengthening
+    scheme: Scheme = Scheme.Classic
+    grid_size: int = 0
+    block_width: int = 0
+    work_factor: int = 0
+    ranks: int = 0
+    steps: int = 0
+    mode: Mode = Mode.VirtualTime
+    avg_us_per_step: float = 0.0
+    setup_us: float = 0.0
+    messages_sent: int = 0
+    bytes_sent: int = 0
+    exchange_rounds: int = 0
+    virtual_comm_us: float = 0.0
+
+    def to_c(self) -> _capi.s1d_record:
+        r = _capi.s1d_record()
+        r.equation, r.method, r.scheme, r.mode = int(self.equation), int(self.method), int(self.scheme), int(
+            self.mode)
+        r.grid_size, r.block_width, r.work_factor, r.ranks, r.steps = (self.grid_size, self.block_width,
+                                                                       self.work_factor, self.ranks, self.steps)
+        r.avg_us_per_step, r.setup_us = self.avg_us_per_step, self.setup_us
+        r.messages_sent, r.bytes_sent, r.exchange_rounds = self.messages_sent, self.bytes_sent, self.exchange_rounds
+        r.virtual_comm_us = self.virtual_comm_us
+        return r
+
+    @staticmethod
+    def from_c(r: _capi.s1d_record) -> "TimingRecord":
+        return TimingRecord(Equation(r.equation), Method(r.method), Scheme(r.scheme), r.grid_size, r.block_width,
+                            r.work_factor, r.ranks, r.steps, Mode(r.mode), r.avg_us_per_step, r.setup_us,
+                            r.messages_sent, r.bytes_sent, r.exchange_rounds, r.virtual_comm_us)
+
+
+@dataclass
+class FitResult:
+    A: float
+    b: float
+    r_squared: float
+
+
+def measure(cfg: LaunchConfig) -> TimingRecord:
+    """sweep1d::measure (src/perf.cpp:29-32) on the B200."""
+    rec = _capi.s1d_record()
+    e = _errbuf()
+    _check(lib().s1d_measure(C.byref(cfg.to_c()), C.byref(rec), e, 1024), e)
+    return TimingRecord.from_c(rec)
+
+
+CSV_HEADER = None
+
+
+def csv_header() -> str:
+    return lib().s1d_csv_header().decode()
+
+
+def csv_row(rec: TimingRecord) -> str:
+    buf = C.create_string_buffer(1024)
+    n = lib().s1d_csv_row(C.byref(rec.to_c()), buf, 1024)
+    if n < 0:
+        raise Sweep1dError("csv row too long")
+    return buf.value.decode()
+
+
+def emit_csv(records: List[TimingRecord], path: str) -> None:
+    arr = (_capi.s1d_record * max(len(records), 1))(*[r.to_c() for r in records])
+    e = _errbuf()
+    _check(lib().s1d_emit_csv(arr, len(records), path.encode(), e, 1024), e)
+
+
+def read_csv(path: str) -> List[TimingRecord]:
+    n = C.c_size_t(0)
+    e = _errbuf()
+    _check(lib().s1d_read_csv(path.encode(), None, 0, C.byref(n), e, 1024), e)
+    arr = (_capi.s1d_record * max(n.value, 1))()
+    _check(lib().s1d_read_csv(path.encode(), arr, n.value, C.byref(n), e, 1024), e)
+    return [TimingRecord.from_c(arr[i]) for i in range(n.value)]
+
+
+def power_law_fit(points) -> FitResult:
+    """Least-squares fit of log(time) vs log(n) (src/perf.cpp:42-82)."""
+    xs = np.ascontiguousarray([p[0] for p in points], dtype=np.float64)
+    ys = np.ascontiguousarray([p[1] for p in points], dtype=np.float64)
+    A, b, r2 = C.c_double(), C.c_double(), C.c_double()
+    e = _errbuf()
+    _check(lib().s1d_power_law_fit(_dptr(xs), _dptr(ys), xs.size, C.byref(A), C.byref(b), C.byref(r2), e, 1024), e)
+    return FitResult(A.value, b.value, r2.value)
+
+
+def best_config(records: List[TimingRecord]) -> TimingRecord:
+    """Fastest record; ties: smaller w, then smaller WF (src/perf.cpp:84-97)."""
+    arr = (_capi.s1d_record * max(len(records), 1))(*[r.to_c() for r in records])
+    i = lib().s1d_best_config(arr, len(records))
+    if i < 0:
+        _raise(-i, "best_config over an empty record set")
+    return records[i]
+
+
+def speedup(time_classic: float, time_swept: float) -> float:
+    return time_classic / time_swept
+
+
+def flattening_speedup(time_lengthening: float, time_flattening: float) -> float:
+    return time_lengthening / time_flattening

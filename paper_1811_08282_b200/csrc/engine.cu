@@ -774,6 +774,33 @@ uint64_t s1d_swept_buffer_cells(uint64_t w, int equation, int method) {
     return w / 2 + static_cast<uint64_t>(s1d::make_spec(equation, method).h);
 }
 
+int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        s1d::Solver solver;
+        solver.init(*cfg);
+        s1d_stats st{};
+        s1d_timing tm{};
+        solver.advance(&st, &tm);
+        const s1d_config& c = solver.cfg;
+        *out = s1d_record{};
+        out->equation = c.equation;
+        out->method = c.method;
+        out->scheme = c.scheme;
+        out->mode = c.mode;
+        out->grid_size = c.grid_size;
+        out->block_width = c.block_width;
+        out->work_factor = c.work_factor;
+        out->ranks = c.ranks;
+        out->steps = c.steps;
+        out->avg_us_per_step = c.steps > 0 ? tm.loop_seconds * 1e6 / static_cast<double>(c.steps) : 0.0;
+        out->setup_us = tm.setup_seconds * 1e6;
+        out->messages_sent = st.messages_sent;
+        out->bytes_sent = st.bytes_sent;
+        out->exchange_rounds = st.exchange_rounds;
+        out->virtual_comm_us = 0.0;
+    });
+}
+
 int s1d_create(const s1d_config* cfg, s1d_solver** out, char* err, size_t errlen) {
     *out = nullptr;
     auto holder = std::make_unique<s1d_solver>();

@@ -94,3 +94,29 @@ def test_solver_handle_repeat_and_custom_state(gpu):
     with s1d.Solver(cfg(s1d.Scheme.Classic, 1 << 12, 64, 100)) as sc:
         want, _, _ = sc.solve(x)
     assert_bitwise(got, want)
+
+
+def test_cli_verify_and_sweep(gpu, tmp_path):
+    import os
+    import subprocess
+    cli = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_1811_08282_b200", "_lib",
+                       "s1d")
+    r = subprocess.run([cli, "verify", "equation=heat", "n=960", "w=16", "ranks=3", "steps=50"], capture_output=True,
+                       text=True)
+    assert r.returncode == 0 and "bitwise: true" in r.stdout, r.stdout + r.stderr
+    r = subprocess.run([cli, "verify", "equation=euler", "method=flattening", "n=2048", "w=32", "steps=40"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0 and "bitwise: true" in r.stdout, r.stdout + r.stderr
+    out = tmp_path / "s.csv"
+    r = subprocess.run([cli, "sweep", "--n", "2^14,2^15,2^16", "--w", "32,64", "--out", str(out), "steps=64"],
+                       capture_output=True, text=True)
+    assert r.returncode == 0, r.stderr
+    recs = s1d.read_csv(str(out))
+    assert len(recs) == 12 and all(x.avg_us_per_step > 0 for x in recs)
+    r = subprocess.run([cli, "fit", str(out), "--scheme", "swept"], capture_output=True, text=True)
+    assert r.returncode == 0 and "swept" in r.stdout
+
+
+def test_measure_record(gpu):
+    t = s1d.measure(cfg(s1d.Scheme.Swept, 1 << 14, 64, 128))
+    assert t.avg_us_per_step > 0 and t.exchange_rounds == 4 and t.scheme == s1d.Scheme.Swept
