@@ -299,6 +299,27 @@ def run_b200(args, rank, world):
                    "hbm_GBps": round(CLASSIC_BYTES_PER_UPDATE * n_per * args.classic_T / ct / 1e9, 1),
                    "swept_speedup": round(value / world / crate, 3)}
 
+    # Secondary configuration (BASELINE configs[2]): Euler Sod, both methods,
+    # swept vs classic on this GPU. Point-update = one point x one time step.
+    euler = None
+    if args.euler and world == 1:
+        euler = {"grid_size": 1 << args.euler_log2n, "block_width": args.euler_w, "steps_per_run": args.euler_T,
+                 "unit": "Mpt-steps/s"}
+        for meth in ("lengthening", "flattening"):
+            for sch in ("swept", "classic"):
+                ecfg = s1d.LaunchConfig(equation=s1d.Equation.Euler,
+                                        method=s1d.Method.Lengthening if meth == "lengthening"
+                                        else s1d.Method.Flattening,
+                                        scheme=s1d.Scheme.Swept if sch == "swept" else s1d.Scheme.Classic,
+                                        grid_size=1 << args.euler_log2n, block_width=args.euler_w, ranks=1,
+                                        steps=args.euler_T if sch == "swept" else max(args.euler_T // 8, 16),
+                                        num_devices=1)
+                with s1d.Solver(ecfg) as es:
+                    es.advance()
+                    best = min(es.advance()[1].loop_seconds for _ in range(2))
+                euler[f"{meth}_{sch}"] = round(ecfg.grid_size * ecfg.steps / best / 1e6, 2)
+            euler[f"{meth}_swept_speedup"] = round(euler[f"{meth}_swept"] / euler[f"{meth}_classic"], 3)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -325,7 +346,7 @@ def run_b200(args, rank, world):
                        "l2": "inputs larger than L2 (1 GiB state per GPU vs 126 MB L2)"},
             "us_per_timestep": round(1e6 * loop_s / args.steps / args.T, 3),
             "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
-            "classic_same_grid": classic, "cpu_baseline": cpu,
+            "classic_same_grid": classic, "euler_sod": euler, "cpu_baseline": cpu,
             "wall_seconds_timed_region": round(wall, 3),
         }
         print(json.dumps(line), flush=True)
@@ -359,6 +380,10 @@ def main(argv=None):
     ap.add_argument("--classic-T", type=int, default=256)
     ap.add_argument("--no-compare-classic", dest="compare_classic", action="store_false")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-euler", dest="euler", action="store_false", help="skip the Euler (configs[2]) lines")
+    ap.add_argument("--euler-log2n", type=int, default=22)
+    ap.add_argument("--euler-w", type=int, default=512)
+    ap.add_argument("--euler-T", type=int, default=1024)
     ap.add_argument("--ref-n", type=int, default=1 << 25, help="CPU reference sample grid size")
     ap.add_argument("--ref-steps", type=int, default=2048, help="CPU reference sample time steps")
     args = ap.parse_args(argv)

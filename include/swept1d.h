@@ -156,6 +156,19 @@ uint64_t s1d_swept_buffer_cells(uint64_t w, int equation, int method);
 int s1d_run(const s1d_config* cfg, double* state_out, size_t state_len, s1d_stats* stats, s1d_timing* timing,
             char* err, size_t errlen);
 
+/* ---- debug run (RunOptions, inc/debug.hpp:17-62) ------------------------- */
+typedef struct s1d_debug {
+    int coverage;            /* count every (point, substep) the kernels compute */
+    int perturb_ulp;         /* nudge the run's first computed value by one ulp (shard 0) */
+    uint32_t* coverage_out;  /* host [steps*S][n] counts, index (substep-1)*n + point */
+    size_t coverage_len;
+} s1d_debug;
+/* s1d_run with instrumented kernels (same geometry and arithmetic; slower).
+ * A correct tiling computes every (point, substep) exactly once
+ * (CoverageCounter::defects() empty). */
+int s1d_run_debug(const s1d_config* cfg, const s1d_debug* dbg, double* state_out, size_t state_len,
+                  s1d_stats* stats, s1d_timing* timing, char* err, size_t errlen);
+
 /* ---- reusable solver handle -------------------------------------------- */
 typedef struct s1d_solver s1d_solver;
 int s1d_create(const s1d_config* cfg, s1d_solver** out, char* err, size_t errlen);

@@ -47,6 +47,11 @@ class s1d_record(C.Structure):
                 ("exchange_rounds", C.c_uint64), ("virtual_comm_us", C.c_double)]
 
 
+class s1d_debug(C.Structure):
+    _fields_ = [("coverage", C.c_int), ("perturb_ulp", C.c_int), ("coverage_out", C.POINTER(C.c_uint32)),
+                ("coverage_len", C.c_size_t)]
+
+
 _dp = C.POINTER(C.c_double)
 _E = [C.c_char_p, C.c_size_t]
 
@@ -72,6 +77,8 @@ SIGNATURES = {
     "s1d_swept_buffer_cells": (C.c_uint64, [C.c_uint64, C.c_int, C.c_int]),
     "s1d_run": (C.c_int, [C.POINTER(s1d_config), _dp, C.c_size_t, C.POINTER(s1d_stats), C.POINTER(s1d_timing)]
                 + _E),
+    "s1d_run_debug": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_debug), _dp, C.c_size_t, C.POINTER(s1d_stats),
+                                C.POINTER(s1d_timing)] + _E),
     "s1d_create": (C.c_int, [C.POINTER(s1d_config), C.POINTER(C.c_void_p)] + _E),
     "s1d_destroy": (None, [C.c_void_p]),
     "s1d_get_config": (C.c_int, [C.c_void_p, C.POINTER(s1d_config)]),

@@ -442,6 +442,46 @@ def run(cfg: LaunchConfig) -> RunResult:
     return RunResult(out, _stats(st, tm.setup_seconds), _timing(tm))
 
 
+@dataclass
+class RunOptions:
+    """sweep1d::RunOptions subset (inc/debug.hpp:17-24) for instrumented runs."""
+    coverage: bool = False
+    perturb_ulp: bool = False
+
+
+@dataclass
+class DebugResult:
+    result: RunResult
+    coverage: Optional[np.ndarray]  # [steps*S, n] counts, or None
+
+    def defects(self):
+        """(substep, point) pairs not computed exactly once (CoverageCounter::defects)."""
+        if self.coverage is None:
+            return []
+        bad = np.argwhere(self.coverage != 1)
+        return [(int(lv) + 1, int(x), int(self.coverage[lv, x])) for lv, x in bad[:100]]
+
+
+def run_debug(cfg: LaunchConfig, opts: RunOptions) -> DebugResult:
+    """s1d_run with the instrumented kernels (tiling coverage counter, 1-ulp
+    mutation hook)."""
+    spec = cfg.spec()
+    out = np.empty(cfg.grid_size * spec.values_per_point, dtype=np.float64)
+    total = cfg.steps * spec.substeps_per_step
+    cov = np.zeros((total, cfg.grid_size), dtype=np.uint32) if opts.coverage else None
+    d = _capi.s1d_debug()
+    d.coverage = int(opts.coverage)
+    d.perturb_ulp = int(opts.perturb_ulp)
+    if cov is not None:
+        d.coverage_out = cov.ctypes.data_as(C.POINTER(C.c_uint32))
+        d.coverage_len = cov.size
+    st, tm = _capi.s1d_stats(), _capi.s1d_timing()
+    e = _errbuf()
+    _check(lib().s1d_run_debug(C.byref(cfg.to_c()), C.byref(d), _dptr(out), out.size, C.byref(st), C.byref(tm), e,
+                               1024), e)
+    return DebugResult(RunResult(out, _stats(st, tm.setup_seconds), _timing(tm)), cov)
+
+
 class Solver:
     """Reusable device-resident solver (s1d_create/s1d_solve/...)."""
 

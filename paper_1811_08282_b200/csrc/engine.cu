@@ -53,6 +53,7 @@ struct Shard {
     double* EL[2] = {nullptr, nullptr};
     double* ER[2] = {nullptr, nullptr};
     unsigned* flags = nullptr; // multi-process: [0] left neighbour's rounds, [1] right's
+    unsigned* cov = nullptr;   // debug runs: coverage counts [total][n]
     int* err = nullptr;
     double* staging = nullptr; // AoS (vpp = 3) upload/download buffer (Euler)
     const double* final_state = nullptr;
@@ -89,6 +90,7 @@ struct Solver {
     int p = 2;
     bool euler = false, flat = false;
     double setup_seconds = 0.0;
+    bool debug = false, perturb = false; // instrumented kernels (s1d_run_debug)
     std::string last_error;
     std::vector<double> host_ic; // initial condition of the local shards (global order within)
 
@@ -112,6 +114,7 @@ struct Solver {
                 cudaFree(s.ER[k]);
             }
             cudaFree(s.flags);
+            cudaFree(s.cov);
             cudaFree(s.err);
             cudaFree(s.staging);
             if (s.ev_start) cudaEventDestroy(s.ev_start);
@@ -394,6 +397,43 @@ struct Solver {
         }
     }
 
+    DebugArgs dbg_args(int g) {
+        DebugArgs d;
+        if (!debug) return d;
+        d.cov = sh(g).cov;
+        d.cov_n = cfg.grid_size;
+        d.gstart = sh(g).start;
+        d.perturb = (perturb && sh(g).start == 0) ? 1 : 0;
+        return d;
+    }
+
+    // Debug run: allocate coverage counters, run, return summed counts.
+    void run_debug(bool coverage, bool nudge, std::uint32_t* host_cov, std::size_t cov_len, s1d_stats* st,
+                   s1d_timing* tm) {
+        debug = true;
+        perturb = nudge;
+        const std::uint64_t total = static_cast<std::uint64_t>(cfg.steps) * static_cast<std::uint64_t>(spec.S);
+        const std::size_t cells = cfg.grid_size * total;
+        if (coverage) {
+            if (!host_cov || cov_len < cells) throw Error(S1D_INVALID_CONFIG, "coverage buffer too small (n*steps*S)");
+            for (int g : locals) {
+                S1D_CUDA(cudaSetDevice(sh(g).dev));
+                S1D_CUDA(cudaMalloc(&sh(g).cov, sizeof(unsigned) * std::max<std::size_t>(cells, 1)));
+                S1D_CUDA(cudaMemset(sh(g).cov, 0, sizeof(unsigned) * std::max<std::size_t>(cells, 1)));
+            }
+        }
+        advance(st, tm);
+        if (coverage) {
+            std::fill(host_cov, host_cov + cells, 0u);
+            std::vector<std::uint32_t> part(cells);
+            for (int g : locals) {
+                S1D_CUDA(cudaSetDevice(sh(g).dev));
+                if (cells) S1D_CUDA(cudaMemcpy(part.data(), sh(g).cov, sizeof(unsigned) * cells, cudaMemcpyDeviceToHost));
+                for (std::size_t i = 0; i < cells; ++i) host_cov[i] += part[i];
+            }
+        }
+    }
+
     void record_all(cudaEvent_t Shard::*ev) {
         for (int g : locals) {
             Shard& s = sh(g);
@@ -432,6 +472,7 @@ struct Solver {
                 a.gamma = cfg.gamma;
                 a.dt_dx = cfg.dt_dx;
                 a.error_flag = s.err;
+                a.dbg = dbg_args(g);
                 S1D_CUDA(cudaSetDevice(s.dev));
                 if (euler) S1D_CUDA(launch_euler_classic(flat ? 1 : 0, a, s.st));
                 else S1D_CUDA(launch_heat_classic(a, s.st));
@@ -478,9 +519,10 @@ struct Solver {
             a.gamma = cfg.gamma;
             a.dt_dx = cfg.dt_dx;
             a.error_flag = s.err;
+            a.dbg = dbg_args(g);
             S1D_CUDA(cudaSetDevice(s.dev));
-            if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, a, s.st));
-            else S1D_CUDA(launch_heat_tile(kind, a, s.st));
+            if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, a, s.st, debug));
+            else S1D_CUDA(launch_heat_tile(kind, a, s.st, debug));
             stats.kernel_launches += 1;
             if (R() > 1 && kind != kUp)
                 stats.edge_bytes_device += sizeof(double) * static_cast<std::uint64_t>(w) * spec.rec;
@@ -772,6 +814,20 @@ int64_t s1d_schedule(int kind, uint64_t w, uint64_t h, int64_t* substep, int64_t
 
 uint64_t s1d_swept_buffer_cells(uint64_t w, int equation, int method) {
     return w / 2 + static_cast<uint64_t>(s1d::make_spec(equation, method).h);
+}
+
+int s1d_run_debug(const s1d_config* cfg, const s1d_debug* dbg, double* state_out, size_t state_len, s1d_stats* stats,
+                  s1d_timing* timing, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        s1d::Solver solver;
+        solver.init(*cfg);
+        if (state_len < solver.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
+        s1d_timing t{};
+        solver.run_debug(dbg && dbg->coverage, dbg && dbg->perturb_ulp, dbg ? dbg->coverage_out : nullptr,
+                         dbg ? dbg->coverage_len : 0, stats, &t);
+        solver.download(state_out, false);
+        if (timing) *timing = t;
+    });
 }
 
 int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen) {

@@ -25,6 +25,7 @@
 #include <cstdlib>
 
 #include "euler_math.cuh"
+#include "device_util.cuh"
 #include "kernels.hpp"
 
 namespace s1d {
@@ -60,6 +61,10 @@ __device__ __forceinline__ Fields fields_of(const ClassicArgs& a) {
     return Fields{a.out, a.N, a.fstride, a.halo_l, a.halo_l_fstride, a.halo_r, a.halo_r_fstride, a.h};
 }
 
+__device__ __forceinline__ void classic_count(const ClassicArgs& a, std::uint64_t x) {
+    atomicAdd(a.dbg.cov + (std::uint64_t)(a.counter - 1) * a.dbg.cov_n + (a.dbg.gstart + x) % a.dbg.cov_n, 1u);
+}
+
 __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
     if (__any_sync(__activemask(), bad) && bad) atomicOr(flag, 1);
 }
@@ -83,8 +88,12 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_len_c
                 sh[0][t] = em::pressure(F.ld(s, x), F.ld(s + 1, x), F.ld(s + 2, x), gamma, bad);
             }
             __syncthreads();
-            for (int t = threadIdx.x; t < nb; t += blockDim.x)
-                a.out[i0 + t + 6 * a.fstride] = em::ratio(sh[0][t], sh[0][t + 1], sh[0][t + 2]);
+            for (int t = threadIdx.x; t < nb; t += blockDim.x) {
+                double pr = em::ratio(sh[0][t], sh[0][t + 1], sh[0][t + 2]);
+                if (a.dbg.perturb && a.counter == 1 && i0 + t == 0) pr = next_up(pr); // debug runs only
+                if (a.dbg.cov) classic_count(a, i0 + t);
+                a.out[i0 + t + 6 * a.fstride] = pr;
+            }
         } else {
             const bool fin = (KIND == 0);
             const int rs = fin ? 3 : 0, ws = fin ? 0 : 3;
@@ -106,6 +115,7 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_len_c
                 for (int k = 0; k < 3; ++k)
                     a.out[x + (ws + k) * a.fstride] =
                         em::update(a.out[x + k * a.fstride], factor, sh[k][t + 1], sh[k][t]);
+                if (a.dbg.cov) classic_count(a, x);
             }
         }
         __syncthreads();
@@ -147,6 +157,8 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_flat_
 #pragma unroll
             for (int k = 0; k < 3; ++k)
                 a.out[x + (ws + k) * a.fstride] = em::update(a.out[x + k * a.fstride], factor, sf[k][t + 1], sf[k][t]);
+            if (a.dbg.perturb && a.counter == 1 && x == 0) a.out[ws * a.fstride] = next_up(a.out[ws * a.fstride]);
+            if (a.dbg.cov) classic_count(a, x);
         }
         __syncthreads();
     }
@@ -202,7 +214,7 @@ inline int euler_tiles_per_cta(int flat, int w) {
     return gt;
 }
 
-template <int FLAT, int KIND>
+template <int FLAT, int KIND, bool DBG>
 __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs a, int GT) {
     using G = TileGeom<FLAT>;
     constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
@@ -228,6 +240,19 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
         const int b = tile_of(gi);
         const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
         return centre - w / 2 - H;
+    };
+    // debug: count (point, counter) computations; nudge the run's first value
+    auto count = [&](int gi, int x, std::int64_t c) {
+        if (DBG && a.dbg.cov) {
+            unsigned* row = a.dbg.cov + (std::uint64_t)(c - 1) * a.dbg.cov_n;
+            atomicAdd(row + (a.dbg.gstart + (std::uint64_t)(origin(gi) + x)) % a.dbg.cov_n, 1u);
+        }
+    };
+    auto perturb = [&](int gi, int x, std::int64_t c, int field) {
+        // reference perturb_one_ulp: the up-triangle's first level at global
+        // point h of shard 0 (tile 0: local x = 2H)
+        if (DBG && KIND == kUp && a.dbg.perturb && c == 1 && tile_of(gi) == 0 && x == 2 * H)
+            S(gi)[field * W2 + x] = next_up(S(gi)[field * W2 + x]);
     };
     // Visit (tile, x) for x in [x0, x1) of every live tile, threads spread
     // over the concatenation of the tiles' ranges.
@@ -319,6 +344,8 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
                 for_all(lo, hi, [&](int gi, int x) {
                     const double* P = Pp(gi);
                     S(gi)[6 * W2 + x] = em::ratio(P[x - 1], P[x], P[x + 1]);
+                    count(gi, x, c);
+                    perturb(gi, x, c, 6);
                 });
                 between(1);
             } else {
@@ -345,6 +372,7 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
                     for (int k = 0; k < 3; ++k)
                         St[(ws + k) * W2 + x] =
                             em::update(St[k * W2 + x], factor, F[k * (W2 + 1) + x + 1], F[k * (W2 + 1) + x]);
+                    count(gi, x, c);
                 });
                 between(1);
             }
@@ -379,6 +407,8 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
                 for (int k = 0; k < 3; ++k)
                     St[(ws + k) * W2 + x] =
                         em::update(St[k * W2 + x], factor, F[k * (W2 + 1) + x + 1], F[k * (W2 + 1) + x]);
+                count(gi, x, c);
+                perturb(gi, x, c, ws);
             });
             between(1);
         }
@@ -436,13 +466,13 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
     raise_flag(a.error_flag, bad);
 }
 
-template <int FLAT>
+template <int FLAT, bool DBG = false>
 cudaError_t launch_tile_f(int kind, const TileArgs& a, cudaStream_t st) {
     const int GT = euler_tiles_per_cta(FLAT, a.w);
     const size_t smem = (size_t)GT * euler_tile_smem(FLAT, a.w);
-    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp>
-                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond>
-                                                        : euler_tile<FLAT, kDown>;
+    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp, DBG>
+                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG>
+                                                        : euler_tile<FLAT, kDown, DBG>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -513,7 +543,8 @@ cudaError_t launch_euler_classic(int flat, const ClassicArgs& a, cudaStream_t st
     return cudaGetLastError();
 }
 
-cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_t st) {
+cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_t st, bool debug) {
+    if (debug) return flat ? launch_tile_f<1, true>(kind, a, st) : launch_tile_f<0, true>(kind, a, st);
     return flat ? launch_tile_f<1>(kind, a, st) : launch_tile_f<0>(kind, a, st);
 }
 

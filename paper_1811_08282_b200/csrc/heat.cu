@@ -28,9 +28,11 @@
 // reloads them with predicated loads (points further out are don't-care:
 // they are outside the dependency cone). Exports L[d], R[d] are written by
 // the owning threads with exactly-predicated stores.
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 
+#include "device_util.cuh"
 #include "kernels.hpp"
 
 namespace s1d {
@@ -55,6 +57,12 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
         double2 o;
         o.x = heat_f(l, c.x, c.y, fo);
         o.y = heat_f(c.x, c.y, r, fo);
+        if (a.dbg.perturb && a.counter == 1 && i == 0) o.x = next_up(o.x); // debug runs only
+        if (a.dbg.cov) {
+            unsigned* row = a.dbg.cov + (std::uint64_t)(a.counter - 1) * a.dbg.cov_n;
+            atomicAdd(row + (a.dbg.gstart + i) % a.dbg.cov_n, 1u);
+            atomicAdd(row + (a.dbg.gstart + i + 1) % a.dbg.cov_n, 1u);
+        }
         reinterpret_cast<double2*>(a.out)[p] = o;
     }
 }
@@ -432,6 +440,124 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
     }
 }
 
+// ---------------------------------------------------------------------------
+// Instrumented tile kernel (debug runs only): the same tile geometry, insert /
+// export rules and arithmetic, run as plain level loops, counting every
+// (point, counter) it computes inside the level's span and optionally nudging
+// the run's first computed value (reference perturb_ulp: the up-triangle's
+// first level, global point h, shard 0).
+// ---------------------------------------------------------------------------
+template <int P, int KIND>
+__global__ void __launch_bounds__(256) heat_tile_debug_kernel(const TileArgs a, int G) {
+    extern __shared__ double sm[];
+    const int w = a.w, m = a.m;
+    const int tt = w / P;
+    const int t = threadIdx.x;
+    const int g = t / tt;
+    const int b = blockIdx.x * G + g;
+    const bool live = b < a.nb;
+    const double fo = a.fourier;
+    TileCtx<P> c;
+    c.w = w;
+    c.m = m;
+    c.tt = tt;
+    c.lt = t - g * tt;
+    c.my_lo = 1 + c.lt * P;
+    c.xs = G * (tt + 2);
+    c.XL = sm;
+    c.XF = sm + 2 * c.xs;
+    c.slot = g * (tt + 2) + c.lt + 1;
+    double* einR = sm + 4 * c.xs + (std::size_t)g * tile_edge_stride(w);
+    double* einL = einR + 2 * kRing;
+    c.einR = einR;
+    c.einL = einL;
+    {
+        const unsigned full = __activemask();
+        c.wlo = __reduce_min_sync(full, c.my_lo);
+        c.whi = __reduce_max_sync(full, c.my_lo + P - 1);
+    }
+    const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
+    const std::int64_t g0 = centre - w / 2 - 1; // shard position of local x = 0
+    auto count = [&](int r, int lo, int hi) {
+        if (!live || !a.dbg.cov) return;
+        unsigned* row = a.dbg.cov + (std::uint64_t)(a.base + r - 1) * a.dbg.cov_n;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const int x = c.my_lo + k;
+            if (x >= lo && x < hi) atomicAdd(row + (a.dbg.gstart + (std::uint64_t)(g0 + x)) % a.dbg.cov_n, 1u);
+        }
+    };
+    double v[P];
+#pragma unroll
+    for (int k = 0; k < P; ++k) v[k] = 0.0;
+    if (KIND == kUp && live) {
+        const double* src = a.state_in + (std::size_t)b * w + (std::size_t)c.lt * P;
+#pragma unroll
+        for (int k = 0; k < P; ++k) v[k] = src[k];
+    }
+    if (KIND != kUp) { // whole edges staged (debug sizes are small)
+        const double* pR = nullptr;
+        const double* pL = nullptr;
+        if (live) {
+            if (a.seam) {
+                pR = a.in_R + (std::size_t)b * w;
+                pL = (b + 1 < a.nb) ? a.in_L + (std::size_t)(b + 1) * w : a.peer_L;
+            } else {
+                pR = (b > 0) ? a.in_R + (std::size_t)(b - 1) * w : a.peer_R;
+                pL = a.in_L + (std::size_t)b * w;
+            }
+        }
+        for (int r = 1; r <= m; ++r) {
+            const int lo = w / 2 + 1 - r, hi = w / 2 + 1 + r;
+            __syncthreads(); // previous level's ring reads done
+            if (live) // stage level r's 2+2 values into the ring slot
+                for (int i = c.lt; i < 4; i += tt) {
+                    const int q = r - 1, j = i & 1;
+                    double* ring = (i < 2 ? einR : einL);
+                    ring[(2 * q + j) & kRingMask] = (i < 2 ? pR : pL)[2 * q + j];
+                }
+            __syncthreads();
+            insert_level(c, v, r, lo, hi);
+            publish(c, v, r);
+            if (r == m) {
+                const int par = (r & 1) * c.xs, base = g * (tt + 2);
+                if (c.lt == 0) c.XL[par + base] = einR[(2 * (m - 1)) & kRingMask];
+                if (c.lt == tt - 1) c.XF[par + base + tt + 1] = einL[(2 * (m - 1) + 1) & kRingMask];
+            }
+            __syncthreads();
+            compute_level(c, v, r, lo, hi, fo);
+            count(r, lo, hi);
+        }
+    }
+    double* oL = a.out_L + (std::size_t)b * w;
+    double* oR = a.out_R + (std::size_t)b * w;
+    if (KIND != kDown) {
+        if (live) export_level(c, v, 0, 1, w + 1, oL, oR);
+        for (int r = m + 1; r <= 2 * m - 1; ++r) {
+            const int d = r - m, lo = 1 + d, hi = 1 + w - d;
+            publish(c, v, r);
+            __syncthreads();
+            compute_level(c, v, r, lo, hi, fo);
+            count(r, lo, hi);
+            if (KIND == kUp && r == m + 1 && a.dbg.perturb && b == 0) {
+                const int x = 2; // global point h = 1 of shard 0 (g0 = -1)
+#pragma unroll
+                for (int k = 0; k < P; ++k)
+                    if (c.my_lo + k == x) v[k] = next_up(v[k]);
+            }
+            if (live) export_level(c, v, d, lo, hi, oL, oR);
+        }
+    } else if (live) {
+        const std::int64_t gp0 = centre - w / 2 + (std::int64_t)c.lt * P;
+#pragma unroll
+        for (int k = 0; k < P; ++k) {
+            const std::uint64_t gp = (std::uint64_t)(gp0 + k);
+            if (gp < a.N) a.state_out[gp] = v[k];
+            else a.state_right[gp - a.N] = v[k];
+        }
+    }
+}
+
 int tiles_per_cta(int w, int p) {
     const int tt = w / p;
     int G = 1;
@@ -487,8 +613,34 @@ cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st) {
+template <int P>
+cudaError_t launch_tile_debug(int kind, const TileArgs& a, cudaStream_t st) {
+    const int tt = a.w / P;
+    const int G = tiles_per_cta(a.w, P);
+    const size_t smem = sizeof(double) * (4 * (size_t)G * (tt + 2) + (size_t)G * tile_edge_stride(a.w));
+    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_debug_kernel<P, kUp>
+                                     : kind == kDiamond ? heat_tile_debug_kernel<P, kDiamond>
+                                                        : heat_tile_debug_kernel<P, kDown>;
+    if (smem > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e != cudaSuccess) return e;
+    }
+    k<<<(unsigned)((a.nb + G - 1) / G), G * tt, smem, st>>>(a, G);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool debug) {
     if (a.w % a.p || a.w / a.p > 1024) return cudaErrorInvalidValue;
+    if (debug) {
+        if (a.w / a.p > 256) return cudaErrorInvalidValue;
+        switch (a.p) {
+        case 2: return launch_tile_debug<2>(kind, a, st);
+        case 4: return launch_tile_debug<4>(kind, a, st);
+        case 8: return launch_tile_debug<8>(kind, a, st);
+        case 16: return launch_tile_debug<16>(kind, a, st);
+        default: return cudaErrorInvalidValue;
+        }
+    }
     if (a.w / a.p > 256) return a.p == 2 ? launch_tile_p<2, 1024>(kind, a, st) : cudaErrorInvalidValue;
     switch (a.p) {
     case 1: return launch_tile_p<1>(kind, a, st);

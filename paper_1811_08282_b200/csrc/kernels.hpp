@@ -9,6 +9,17 @@ namespace s1d {
 
 enum TileKind : int { kUp = 0, kDiamond = 1, kDown = 2 };
 
+// Debug instrumentation (debug builds of the kernels only; RunOptions,
+// inc/debug.hpp:17-62): `cov` counts every (global point, substep) the
+// kernel computes, cov[(counter-1)*cov_n + (gstart + pos) mod cov_n];
+// `perturb` nudges the first value the run computes by one ulp.
+struct DebugArgs {
+    unsigned* cov = nullptr;
+    std::uint64_t cov_n = 0;
+    std::uint64_t gstart = 0; // global index of shard position 0
+    int perturb = 0;          // 1: nudge (shard 0 only)
+};
+
 // One swept phase over the tiles of a shard.
 // Local tile coordinates x in [0, w+2h) map to shard position
 // g = centre - w/2 - h + x. Registers hold x in [h, w+h).
@@ -37,6 +48,7 @@ struct TileArgs {
     // physics
     double fourier = 0.4, gamma = 1.4, dt_dx = 0.0;
     int* error_flag = nullptr;      // device NonPhysicalState flag (Euler)
+    DebugArgs dbg;
 };
 
 struct ClassicArgs {
@@ -53,16 +65,18 @@ struct ClassicArgs {
     std::uint64_t halo_l_fstride = 0, halo_r_fstride = 0;
     double fourier = 0.4, gamma = 1.4, dt_dx = 0.0;
     int* error_flag = nullptr;
+    DebugArgs dbg;
 };
 
+// `debug` selects the instrumented instantiation (coverage / perturb).
 cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st);
-cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st);
+cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool debug = false);
 int heat_points_per_thread(int w);
 
 // Euler (flat = 0 lengthening, 1 flattening). Classic kernels update `out`
 // in place (fields written by a substep are never read by it).
 cudaError_t launch_euler_classic(int flat, const ClassicArgs& a, cudaStream_t st);
-cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_t st);
+cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_t st, bool debug = false);
 cudaError_t launch_euler_unpack(const double* aos, double* st_fields, std::uint64_t N, std::uint64_t fs, int rec,
                                 cudaStream_t st);
 cudaError_t launch_euler_pack(const double* st_fields, double* aos, std::uint64_t N, std::uint64_t fs,

@@ -5,7 +5,7 @@
 #  3. ncu --set full of one Diamond launch (the dominant kernel)
 set -e
 export PYTHONPATH=.
-ARGS=${ARGS:-"--steps 2 --warmup 3 --no-cpu-baseline --e2e-steps 1"}
+ARGS=${ARGS:-"--steps 2 --warmup 3 --no-cpu-baseline --no-euler --e2e-steps 1"}
 python bench.py $ARGS > gpurun_out/prof_plain.log 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
     python bench.py $ARGS > gpurun_out/prof_launches.log 2>&1 || true
