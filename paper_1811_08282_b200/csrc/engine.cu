@@ -54,6 +54,9 @@ struct Shard {
     double* ER[2] = {nullptr, nullptr};
     unsigned* flags = nullptr; // multi-process: [0] left neighbour's rounds, [1] right's
     unsigned* cov = nullptr;   // debug runs: coverage counts [total][n]
+    cudaStream_t cs = nullptr; // copy stream for pipelined host I/O (s1d_solve)
+    std::vector<cudaEvent_t> ev_h2d, ev_dn; // per I/O chunk
+    cudaEvent_t ev_fin = nullptr;           // final-slice D2H ordering
     int* err = nullptr;
     double* staging = nullptr; // AoS (vpp = 3) upload/download buffer (Euler)
     const double* final_state = nullptr;
@@ -91,6 +94,15 @@ struct Solver {
     bool euler = false, flat = false;
     double setup_seconds = 0.0;
     bool debug = false, perturb = false; // instrumented kernels (s1d_run_debug)
+    // Pipelined host I/O (s1d_solve): H2D of chunk k overlaps the UpTriangle
+    // of chunk k-1, D2H of chunk k overlaps the DownTriangle of chunk k+1.
+    struct PipeIO {
+        const double* in = nullptr;
+        double* out = nullptr;
+        bool local = false;
+        int K = 1;
+    };
+    PipeIO* pio = nullptr;
     std::string last_error;
     std::vector<double> host_ic; // initial condition of the local shards (global order within)
 
@@ -122,6 +134,10 @@ struct Solver {
             if (s.ev_done) cudaEventDestroy(s.ev_done);
             if (s.ev_dom0) cudaEventDestroy(s.ev_dom0);
             if (s.ev_dom1) cudaEventDestroy(s.ev_dom1);
+            for (cudaEvent_t e : s.ev_h2d) cudaEventDestroy(e);
+            for (cudaEvent_t e : s.ev_dn) cudaEventDestroy(e);
+            if (s.ev_fin) cudaEventDestroy(s.ev_fin);
+            if (s.cs) cudaStreamDestroy(s.cs);
             if (s.st) cudaStreamDestroy(s.st);
         }
         shards.clear();
@@ -397,6 +413,40 @@ struct Solver {
         }
     }
 
+    std::pair<int, int> chunk_tiles(const Shard& s, int k, int K) const {
+        const int nb = static_cast<int>(s.nb);
+        return {static_cast<int>((static_cast<long long>(nb) * k) / K),
+                static_cast<int>((static_cast<long long>(nb) * (k + 1)) / K)};
+    }
+
+    void ensure_pipe(Shard& s, int K) {
+        S1D_CUDA(cudaSetDevice(s.dev));
+        if (!s.cs) S1D_CUDA(cudaStreamCreateWithFlags(&s.cs, cudaStreamNonBlocking));
+        if (!s.ev_fin) S1D_CUDA(cudaEventCreateWithFlags(&s.ev_fin, cudaEventDisableTiming));
+        while (static_cast<int>(s.ev_h2d.size()) < K) {
+            cudaEvent_t a, b;
+            S1D_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
+            S1D_CUDA(cudaEventCreateWithFlags(&b, cudaEventDisableTiming));
+            s.ev_h2d.push_back(a);
+            s.ev_dn.push_back(b);
+        }
+    }
+
+    // D2H (Euler: pack first) of shard positions [p0, p1) once `after` is done.
+    void chunk_d2h(Shard& s, std::uint64_t p0, std::uint64_t p1, cudaEvent_t after) {
+        double* dst = pio->out + (pio->local ? 0 : s.start * spec.vpp) + p0 * spec.vpp;
+        if (!euler) {
+            S1D_CUDA(cudaStreamWaitEvent(s.cs, after, 0));
+            S1D_CUDA(cudaMemcpyAsync(dst, s.state[0] + p0, sizeof(double) * (p1 - p0), cudaMemcpyDeviceToHost, s.cs));
+        } else {
+            S1D_CUDA(launch_euler_pack(s.state[0] + p0, s.staging + 3 * p0, p1 - p0, s.fstride, s.st));
+            S1D_CUDA(cudaEventRecord(after, s.st));
+            S1D_CUDA(cudaStreamWaitEvent(s.cs, after, 0));
+            S1D_CUDA(cudaMemcpyAsync(dst, s.staging + 3 * p0, sizeof(double) * 3 * (p1 - p0), cudaMemcpyDeviceToHost,
+                                     s.cs));
+        }
+    }
+
     DebugArgs dbg_args(int g) {
         DebugArgs d;
         if (!debug) return d;
@@ -521,9 +571,40 @@ struct Solver {
             a.error_flag = s.err;
             a.dbg = dbg_args(g);
             S1D_CUDA(cudaSetDevice(s.dev));
-            if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, a, s.st, debug));
-            else S1D_CUDA(launch_heat_tile(kind, a, s.st, debug));
-            stats.kernel_launches += 1;
+            auto launch = [&](const TileArgs& ta) {
+                if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, ta, s.st, debug));
+                else S1D_CUDA(launch_heat_tile(kind, ta, s.st, debug));
+                stats.kernel_launches += 1;
+            };
+            if (pio && (kind == kUp || kind == kDown)) {
+                const int K = pio->K;
+                const std::uint64_t wu = static_cast<std::uint64_t>(w);
+                for (int k = 0; k < K; ++k) {
+                    const auto [t0, t1] = chunk_tiles(s, k, K);
+                    TileArgs ta = a;
+                    ta.b0 = t0;
+                    ta.b1 = t1;
+                    if (kind == kUp) { // this chunk's initial state has landed
+                        S1D_CUDA(cudaStreamWaitEvent(s.st, s.ev_h2d[static_cast<std::size_t>(k)], 0));
+                        if (euler)
+                            S1D_CUDA(launch_euler_unpack(s.staging + 3 * t0 * wu, s.ic + t0 * wu, (t1 - t0) * wu,
+                                                         s.fstride, spec.rec, s.st));
+                        launch(ta);
+                    } else {
+                        launch(ta);
+                        // Final state written by chunk k: centred tiles write their
+                        // own blocks; seam-centred tiles (odd last cycle) write
+                        // [t0 w + w/2, t1 w + w/2) (the part >= N lands in the
+                        // right shard; this shard's first w/2 come from the left).
+                        S1D_CUDA(cudaEventRecord(s.ev_dn[static_cast<std::size_t>(k)], s.st));
+                        const std::uint64_t p0 = a.seam ? t0 * wu + wu / 2 : t0 * wu;
+                        const std::uint64_t p1 = std::min<std::uint64_t>(a.seam ? t1 * wu + wu / 2 : t1 * wu, s.N);
+                        if (p1 > p0) chunk_d2h(s, p0, p1, s.ev_dn[static_cast<std::size_t>(k)]);
+                    }
+                }
+            } else {
+                launch(a);
+            }
             if (R() > 1 && kind != kUp)
                 stats.edge_bytes_device += sizeof(double) * static_cast<std::uint64_t>(w) * spec.rec;
         }
@@ -585,7 +666,23 @@ struct Solver {
             S1D_CUDA(cudaSetDevice(s.dev));
             S1D_CUDA(cudaEventRecord(s.ev_stop, s.st));
         }
+        if (pio && (cycles & 1)) {
+            // seam-centred last cycle: each shard's first w/2 points are written
+            // by its left neighbour's last tile (that shard's stream; in
+            // multi-process mode the final flag wait above covers it)
+            for (int g : locals) {
+                Shard& s = sh(g);
+                S1D_CUDA(cudaSetDevice(s.dev));
+                if (!mp) S1D_CUDA(cudaStreamWaitEvent(s.st, left_of(g).ev_stop, 0));
+                S1D_CUDA(cudaEventRecord(s.ev_fin, s.st));
+                chunk_d2h(s, 0, cfg.block_width / 2, s.ev_fin);
+            }
+        }
         sync_all();
+        for (int g : locals) {
+            S1D_CUDA(cudaSetDevice(sh(g).dev));
+            if (sh(g).cs) S1D_CUDA(cudaStreamSynchronize(sh(g).cs));
+        }
         float worst_ms = 0.0f, dom_ms = 0.0f;
         const bool have_dom = dom_diamond || dom_classic || dom_updown;
         int flag = 0;
@@ -645,6 +742,59 @@ struct Solver {
             }
             std::snprintf(timing_out->dominant_kernel, sizeof(timing_out->dominant_kernel), "%s", name);
         }
+    }
+
+    // s1d_solve with host copies overlapped with the Up/Down phases (swept,
+    // aligned totals); otherwise upload, advance, download in sequence.
+    void solve(const double* host_in, double* host_out, s1d_stats* st, s1d_timing* tm) {
+        const std::int64_t total = cfg.steps * spec.S;
+        const std::int64_t cycles = cfg.scheme == S1D_SWEPT ? total / static_cast<std::int64_t>(m) : 0;
+        const bool aligned = cycles >= 1 && total == cycles * static_cast<std::int64_t>(m);
+        const auto t0 = std::chrono::steady_clock::now();
+        if (!aligned || debug) {
+            upload(host_in, local_io());
+            sync_all();
+            const auto t1 = std::chrono::steady_clock::now();
+            advance(st, tm);
+            const auto t2 = std::chrono::steady_clock::now();
+            download(host_out, local_io());
+            tm->h2d_seconds = std::chrono::duration<double>(t1 - t0).count();
+            tm->d2h_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
+            return;
+        }
+        PipeIO io;
+        io.in = host_in;
+        io.out = host_out;
+        io.local = local_io();
+        std::uint64_t min_nb = ~0ull;
+        for (int g : locals) min_nb = std::min<std::uint64_t>(min_nb, sh(g).nb);
+        io.K = static_cast<int>(std::min<std::uint64_t>(8, min_nb));
+        sync_all();
+        for (int g : locals) {
+            Shard& s = sh(g);
+            ensure_pipe(s, io.K);
+            const std::uint64_t wu = cfg.block_width;
+            const double* src = host_in + (io.local ? 0 : s.start * spec.vpp);
+            for (int k = 0; k < io.K; ++k) {
+                const auto [a0, a1] = chunk_tiles(s, k, io.K);
+                const std::uint64_t p0 = a0 * wu, p1 = a1 * wu;
+                double* dst = euler ? s.staging + 3 * p0 : s.ic + p0;
+                S1D_CUDA(cudaMemcpyAsync(dst, src + p0 * spec.vpp, sizeof(double) * (p1 - p0) * spec.vpp,
+                                         cudaMemcpyHostToDevice, s.cs));
+                S1D_CUDA(cudaEventRecord(s.ev_h2d[static_cast<std::size_t>(k)], s.cs));
+            }
+        }
+        pio = &io;
+        try {
+            advance(st, tm);
+        } catch (...) {
+            pio = nullptr;
+            throw;
+        }
+        pio = nullptr;
+        tm->h2d_seconds = 0.0; // overlapped with the UpTriangle
+        tm->d2h_seconds = 0.0; // overlapped with the DownTriangle
+        (void)t0;
     }
 
     // Points (x vpp) the host I/O of this solver covers: the global array
@@ -907,16 +1057,7 @@ int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_
             throw s1d::Error(S1D_INVALID_CONFIG, "initial state length mismatch");
         if (out_len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
         s1d_timing t{};
-        const auto t0 = std::chrono::steady_clock::now();
-        s->impl.upload(host_in ? host_in : s->impl.host_ic.data(), s->impl.local_io());
-        s->impl.sync_all();
-        const auto t1 = std::chrono::steady_clock::now();
-        s->impl.advance(stats, &t);
-        const auto t2 = std::chrono::steady_clock::now();
-        s->impl.download(host_out, s->impl.local_io());
-        const auto t3 = std::chrono::steady_clock::now();
-        t.h2d_seconds = std::chrono::duration<double>(t1 - t0).count();
-        t.d2h_seconds = std::chrono::duration<double>(t3 - t2).count();
+        s->impl.solve(host_in ? host_in : s->impl.host_ic.data(), host_out, stats, &t);
         if (timing) *timing = t;
     });
 }

@@ -234,8 +234,8 @@ __global__ void __launch_bounds__(256, S1D_EULER_MINB) euler_tile(const TileArgs
     const std::size_t tstride = (std::size_t)w * REC; // edge doubles per tile per side
     bool bad = false;
 
-    auto tile_of = [&](int gi) { return (int)blockIdx.x * GT + gi; };
-    auto live = [&](int gi) { return tile_of(gi) < a.nb; };
+    auto tile_of = [&](int gi) { return a.b0 + (int)blockIdx.x * GT + gi; };
+    auto live = [&](int gi) { return tile_of(gi) < (a.b1 < 0 ? a.nb : a.b1); };
     auto origin = [&](int gi) { // shard position of local x = 0
         const int b = tile_of(gi);
         const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
@@ -485,7 +485,9 @@ cudaError_t launch_tile_f(int kind, const TileArgs& a, cudaStream_t st) {
     if (nt > cap) nt = cap;
     const int need = 32 * ((2 * TileGeom<FLAT>::CHUNKS * GT + 31) / 32); // feeder threads
     if (nt < need) nt = need;
-    const unsigned grid = (unsigned)((a.nb + GT - 1) / GT);
+    const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
+    if (count <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((count + GT - 1) / GT);
     k<<<grid, nt, smem, st>>>(a, GT);
     return cudaGetLastError();
 }

@@ -334,8 +334,8 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
     const int tt = w / P;                 // threads per tile
     const int t = threadIdx.x;
     const int g = t / tt;                 // tile within the CTA
-    const int b = blockIdx.x * G + g;     // tile index in the shard
-    const bool live = b < a.nb;
+    const int b = a.b0 + blockIdx.x * G + g; // tile index in the shard
+    const bool live = b < (a.b1 < 0 ? a.nb : a.b1);
     const double fo = a.fourier;
 
     TileCtx<P> c;
@@ -454,8 +454,8 @@ __global__ void __launch_bounds__(256) heat_tile_debug_kernel(const TileArgs a, 
     const int tt = w / P;
     const int t = threadIdx.x;
     const int g = t / tt;
-    const int b = blockIdx.x * G + g;
-    const bool live = b < a.nb;
+    const int b = a.b0 + blockIdx.x * G + g;
+    const bool live = b < (a.b1 < 0 ? a.nb : a.b1);
     const double fo = a.fourier;
     TileCtx<P> c;
     c.w = w;
@@ -579,7 +579,9 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    const unsigned grid = (unsigned)((a.nb + G - 1) / G);
+    const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
+    if (count <= 0) return cudaSuccess;
+    const unsigned grid = (unsigned)((count + G - 1) / G);
     k<<<grid, nt, smem, st>>>(a, G);
     return cudaGetLastError();
 }
@@ -625,7 +627,9 @@ cudaError_t launch_tile_debug(int kind, const TileArgs& a, cudaStream_t st) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
-    k<<<(unsigned)((a.nb + G - 1) / G), G * tt, smem, st>>>(a, G);
+    const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
+    if (count <= 0) return cudaSuccess;
+    k<<<(unsigned)((count + G - 1) / G), G * tt, smem, st>>>(a, G);
     return cudaGetLastError();
 }
 

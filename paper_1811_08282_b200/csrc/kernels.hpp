@@ -25,7 +25,8 @@ struct DebugArgs {
 // g = centre - w/2 - h + x. Registers hold x in [h, w+h).
 struct TileArgs {
     int w = 0, h = 1, m = 0;  // block width, half width, levels per half cycle
-    int nb = 0;               // tiles in this launch (= blocks of the shard)
+    int nb = 0;               // tiles of the shard (blocks)
+    int b0 = 0, b1 = -1;      // this launch covers shard tiles [b0, b1) (b1 < 0: all)
     int seam = 0;             // 1: centres at (b+1)w (odd cycles); 0: bw + w/2
     int p = 2;                // points per thread
     std::int64_t base = 0;    // counter of level r is base + r

@@ -120,3 +120,22 @@ def test_cli_verify_and_sweep(gpu, tmp_path):
 def test_measure_record(gpu):
     t = s1d.measure(cfg(s1d.Scheme.Swept, 1 << 14, 64, 128))
     assert t.avg_us_per_step > 0 and t.exchange_rounds == 4 and t.scheme == s1d.Scheme.Swept
+
+
+@pytest.mark.parametrize("eq,method,n,w,steps", [("heat", "lengthening", 1 << 14, 64, 64), ("heat", "lengthening", 1 << 14, 64, 96),
+                                                ("heat", "lengthening", 96 * 64, 64, 32 * 5), ("euler", "lengthening", 1 << 12, 64, 64),
+                                                ("euler", "flattening", 1 << 12, 64, 48), ("euler", "lengthening", 1 << 12, 32, 8 * 3)])
+def test_pipelined_solve_matches_oracle(gpu, eq, method, n, w, steps):
+    # s1d_solve overlaps H2D with the UpTriangle and D2H with the DownTriangle
+    # (aligned totals, both odd and even cycle counts)
+    c = s1d.LaunchConfig(equation=s1d.Equation.Heat if eq == "heat" else s1d.Equation.Euler,
+                         method=s1d.Method.Lengthening if method == "lengthening" else s1d.Method.Flattening,
+                         scheme=s1d.Scheme.Swept, grid_size=n, block_width=w, ranks=1, steps=steps)
+    want = O.port_run_serial(eq, method, n=n, steps=steps)
+    with s1d.Solver(c) as sv:
+        for _ in range(2):
+            got, _, _ = sv.solve()
+            assert_bitwise(got, want)
+        x = O.port_initial_condition("uniform", n, eq)
+        got, _, _ = sv.solve(x)
+        assert_bitwise(got, x)
