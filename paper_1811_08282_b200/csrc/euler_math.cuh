@@ -25,7 +25,22 @@ namespace em {
 __device__ __forceinline__ double add(double a, double b) { return __dadd_rn(a, b); }
 __device__ __forceinline__ double sub(double a, double b) { return __dsub_rn(a, b); }
 __device__ __forceinline__ double mul(double a, double b) { return __dmul_rn(a, b); }
-__device__ __forceinline__ double dvd(double a, double b) { return __ddiv_rn(a, b); }
+// IEEE division with the two special cases the Sod problem hits constantly
+// resolved inline: 0/x (zero momentum on the plateaus) and NaN operands (the
+// degenerate-ratio sentinel, 1/Pr). __ddiv_rn sends both to its out-of-line
+// slow path (a third of all executed instructions before this). Results are
+// bit-identical: 0/x (x finite, nonzero) is a zero whose sign is the XOR of
+// the operand signs, and any NaN operand yields a NaN (payloads never reach a
+// non-NaN value: a NaN ratio only feeds minmod, which returns 0).
+__device__ __forceinline__ double dvd(double a, double b) {
+    const long long ab = __double_as_longlong(a), bb = __double_as_longlong(b);
+    const long long bm = bb & 0x7fffffffffffffffLL;
+    if ((ab & 0x7fffffffffffffffLL) == 0 && bm != 0 && bm < 0x7ff0000000000000LL)
+        return __longlong_as_double((ab ^ bb) & (long long)0x8000000000000000ULL);
+    if (a != a) return a;
+    if (b != b) return b;
+    return __ddiv_rn(a, b);
+}
 
 // (g-1)*(E - ((0.5*m)*m)/rho); non-physical when !(rho > 0) or !(p > 0).
 __device__ __forceinline__ double pressure(double rho, double mom, double ene, double gamma, bool& bad) {
