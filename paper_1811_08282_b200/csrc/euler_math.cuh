@@ -41,10 +41,23 @@ __device__ __forceinline__ double dvd(double a, double b) {
     if (b != b) return b;
     return __ddiv_rn(a, b);
 }
+// Call-site specialisations (same results as dvd): zero dividend with a
+// positive finite divisor (momentum / density on the plateaus; density is
+// checked positive by the caller's physicality test or is a sqrt sum), and
+// a possibly-NaN divisor with dividend 1 (1/Pr).
+__device__ __forceinline__ double dvd_z(double a, double b) {
+    if (a == 0.0 && b > 0.0 && b < __longlong_as_double(0x7ff0000000000000LL))
+        return __longlong_as_double(__double_as_longlong(a) & (long long)0x8000000000000000ULL);
+    return __ddiv_rn(a, b);
+}
+__device__ __forceinline__ double rcp_n(double b) {
+    if (b != b) return b;
+    return __ddiv_rn(1.0, b);
+}
 
 // (g-1)*(E - ((0.5*m)*m)/rho); non-physical when !(rho > 0) or !(p > 0).
 __device__ __forceinline__ double pressure(double rho, double mom, double ene, double gamma, bool& bad) {
-    const double p = mul(sub(gamma, 1.0), sub(ene, dvd(mul(mul(0.5, mom), mom), rho)));
+    const double p = mul(sub(gamma, 1.0), sub(ene, dvd_z(mul(mul(0.5, mom), mom), rho)));
     bad |= !(rho > 0.0) || !(p > 0.0);
     return p;
 }
@@ -60,13 +73,13 @@ __device__ __forceinline__ double ratio(double pl, double pc, double pr) {
     const double apc = fabs(pc), apr = fabs(pr);
     const double scale = apc < apr ? apr : apc;
     if (fabs(den) <= mul(1e-14, scale)) return __longlong_as_double(0x7ff8000000000000LL); // quiet NaN
-    return dvd(sub(pc, pl), den);
+    return dvd(sub(pc, pl), den); // 0/den on one-sided plateaus
 }
 
 // Reconstructed Rusanov flux between cells L and R with stored ratios.
 __device__ __forceinline__ void iflux(double lr, double lm, double le, double rr, double rm, double re, double pr_l,
                                       double pr_r, double gamma, double& f0, double& f1, double& f2, bool& bad) {
-    const double inv_r = dvd(1.0, pr_r);
+    const double inv_r = rcp_n(pr_r);
     const double d0 = sub(rr, lr), d1 = sub(rm, lm), d2 = sub(re, le);
     // recon_l = ql + 0.5*minmod(d, pr_l*d); recon_r = qr - 0.5*minmod(d, (1/pr_r)*d)
     const double al = add(lr, mul(0.5, minmod(d0, mul(pr_l, d0))));
@@ -79,14 +92,14 @@ __device__ __forceinline__ void iflux(double lr, double lm, double le, double rr
     const double pr = pressure(br, bm, be, gamma, bad);
     // Roe-averaged |u| + c
     const double srl = __dsqrt_rn(al), srr = __dsqrt_rn(br);
-    const double inv = dvd(1.0, add(srl, srr));
-    const double u = mul(add(mul(srl, dvd(am, al)), mul(srr, dvd(bm, br))), inv);
-    const double e = mul(add(mul(srl, dvd(ae, al)), mul(srr, dvd(be, br))), inv);
+    const double ul = dvd_z(am, al), ur = dvd_z(bm, br); // also the physical fluxes' u
+    const double inv = __ddiv_rn(1.0, add(srl, srr));
+    const double u = mul(add(mul(srl, ul), mul(srr, ur)), inv);
+    const double e = mul(add(mul(srl, __ddiv_rn(ae, al)), mul(srr, __ddiv_rn(be, br))), inv);
     const double por = mul(sub(gamma, 1.0), sub(e, mul(mul(0.5, u), u)));
     bad |= !(por > 0.0);
     const double lam = add(fabs(u), __dsqrt_rn(mul(gamma, por)));
     // physical fluxes
-    const double ul = dvd(am, al), ur = dvd(bm, br);
     const double fl0 = am, fl1 = add(mul(am, ul), pl), fl2 = mul(add(ae, pl), ul);
     const double fr0 = bm, fr1 = add(mul(bm, ur), pr), fr2 = mul(add(be, pr), ur);
     // 0.5*(fl + fr) - 0.5*(lam*(recon_r - recon_l))
