@@ -3,7 +3,7 @@
 //   heat_classic_kernel   one substep per launch, the naive comparison and the
 //                         swept pad (reference classic_worker,
 //                         engines_impl.hpp:201-213)
-//   heat_tile_kernel<P,K> one swept phase: K = Up (UpTriangle,
+//   heat_tile_kernel<Q,K> one swept phase: K = Up (UpTriangle,
 //                         engines_impl.hpp:280-291), Diamond (:293-307) or
 //                         Down (DownTriangle, last cycle). Boundary tiles read
 //                         their neighbour shard's edge directly (SplitDiamond).
@@ -13,21 +13,20 @@
 // evaluated with explicit round-to-nearest intrinsics so no FMA contraction
 // can change a bit (the reference builds with -ffp-contract=off).
 //
-// Tile layout: a CTA runs G tiles side by side;
-// tile thread lt owns P consecutive points of the w-point core in registers
-// (local x = 1 + lt*P + k, x in [1, w]). Per level a thread publishes its
-// first/last value to shared memory, one barrier, and computes its P points
-// from registers plus the two neighbour values. Warps whose points lie
-// outside the level's span skip the arithmetic (the diamond grows/shrinks by
-// one point per side per level).
+// Production tiles (heat_tile_kernel<Q,K>) use
+// the folded slot-major layout described above the kernel: each thread holds
+// Q = P/2 point pairs symmetric about the tile centre, so the busy threads of
+// every level are a prefix of warps. Per level: publish first/last pair to
+// shared memory, one barrier, 5P FP64 ops from registers.
 //
 // Edges: the left producer's R edges and the right producer's L edges (2
 // values per level each) stream into a small shared-memory ring per tile
-// (cp.async, kRing-2 levels ahead). The insert of level r lands at x = lo-1, lo (left) and hi-1, hi (right); its
-// shared-memory address is affine in x, so the warp that holds those points
-// reloads them with predicated loads (points further out are don't-care:
-// they are outside the dependency cone). Exports L[d], R[d] are written by
-// the owning threads with exactly-predicated stores.
+// (cp.async, kRing-2 levels ahead); inserts reload the two entering
+// distances per side, exports store the two leaving ones.
+//
+// The instrumented debug kernel (heat_tile_debug_kernel) keeps an
+// independent contiguous layout (thread lt owns x = 1 + lt*P + k) with plain
+// level loops, so debug runs cross-check the production geometry.
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -69,16 +68,12 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
 
 // Incoming edges stream through a per-tile ring of kRing levels (2 values per
 // level per side) filled with cp.async kRing-2 levels ahead of use, so shared
-// memory per tile is O(1) in w. Ring index of (level r, x) is affine in x and
-// wrapped with a mask, so predicated insert loads stay contiguous.
+// memory per tile is O(1) in w. The ring index of (level r, x) is affine in x
+// and wrapped with a mask.
 constexpr int kRing = 32;             // levels held per side (power of two)
 constexpr int kRingMask = 2 * kRing - 1;
 __host__ __device__ inline int tile_edge_stride(int) { return 4 * kRing; }
 
-__device__ __forceinline__ void cp_async16(double* smem_dst, const double* gsrc) {
-    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(d), "l"(gsrc) : "memory");
-}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
@@ -173,234 +168,266 @@ __device__ __forceinline__ void insert_level(const TileCtx<P>& c, double (&v)[P]
 #endif
 
 // ---------------------------------------------------------------------------
-// Level loops in segments. Over a phase each warp's role changes only at a
-// handful of levels (the span edges sweep across it once), so the levels are
-// run in segments with compile-time role flags: an idle warp costs a barrier
-// per level, a computing warp publish + barrier + 5P FP64 ops.
+// Production tile kernel: folded, slot-major layout.
+//
+// A tile's core x in [1, w] is folded about its centre (between x = w/2 and
+// w/2+1): distance d pairs the left point x = w/2-d with the right point
+// x = w/2+1+d. Every level's span is a distance prefix — [0, r) expanding,
+// [0, m-d) contracting — so slot s (distances [sQ, sQ+Q), Q = P/2, both
+// sides in registers vl[], vr[]) is busy exactly while sQ lies inside it.
+// Thread t = s*G + g (g = tile in the CTA): a warp holds one slot of 32 tiles
+// (G >= 32) or a few consecutive slots, so the busy threads are a prefix of
+// warps and whole warps drop out as the span shrinks; no warp straddles a
+// span edge on each side as in a contiguous x layout.
+//
+// Inserts (expanding level r: left R[r-1] = (x=lo-1, lo) = left distances
+// (r, r-1); right L[r-1] = (x=hi-1, hi) = right distances (r-1, r)) and
+// exports (contracting d: L[d] = left (m-1-d, m-2-d), R[d] = right
+// (m-2-d, m-1-d), where "distance -1" is the other side's distance 0) fall in
+// one slot row. Per level a thread publishes its first and last pair
+// (double2) to shared memory, one barrier, then 5P FP64 ops from registers.
+// Edge rings are tile-minor ([level*2+j][G], XOR-swizzled) so a slot row's
+// insert reads hit distinct banks.
 // ---------------------------------------------------------------------------
-template <int P>
-__device__ __forceinline__ void compute_span(const TileCtx<P>& c, double (&v)[P], int r, double fo) {
+__device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(smem_dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
+}
+
+// Ring element i (edge value index 2*level+j, wrapped) of tile g; G is a power of two.
+__device__ __forceinline__ int ridx(int i, int g, int G) {
+    i &= kRingMask;
+    return i * G + (g ^ (i & (G - 1)));
+}
+
+template <int Q>
+struct Fold {
+    int m, G, s, g;      // levels, tiles per CTA, slot, tile in CTA
+    int sa, sb;          // slot range of my warp (warp-uniform)
+    double2* F;          // [2][(tt+2)G]: (vl[0], vr[0]) of slot s at (s+1)G+g
+    double2* Lst;        // [2][(tt+2)G]: (vl[Q-1], vr[Q-1]) of slot s at (s+1)G+g
+    int xs;              // parity stride (double2 elements)
+    const double* ringR; // left producer's R edges
+    const double* ringL; // right producer's L edges
+};
+
+template <int Q>
+__device__ __forceinline__ void fpublish(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int r) {
+    const int i = (r & 1) * c.xs + (c.s + 1) * c.G + c.g;
+    c.F[i] = make_double2(vl[0], vr[0]);
+    c.Lst[i] = make_double2(vl[Q - 1], vr[Q - 1]);
+}
+
+template <int Q>
+__device__ __forceinline__ void fcompute(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r, double fo) {
     const int par = (r & 1) * c.xs;
-    const double lft = c.XL[par + c.slot - 1];
-    const double rgt = c.XF[par + c.slot + 1];
-    double nv[P];
-    if (P == 1) {
-        nv[0] = heat_f(lft, v[0], rgt, fo);
-    } else {
-        nv[0] = heat_f(lft, v[0], v[1], fo);
+    const double2 in = c.Lst[par + c.s * c.G + c.g];      // slot s-1: distance sQ-1
+    const double2 out = c.F[par + (c.s + 2) * c.G + c.g]; // slot s+1: distance sQ+Q
+    const double inL = c.s == 0 ? vr[0] : in.x;           // x+1 of left distance sQ
+    const double inR = c.s == 0 ? vl[0] : in.y;           // x-1 of right distance sQ
+    double nl[Q], nr[Q];
 #pragma unroll
-        for (int k = 1; k < P - 1; ++k) nv[k] = heat_f(v[k - 1], v[k], v[k + 1], fo);
-        nv[P - 1] = heat_f(v[P - 2], v[P - 1], rgt, fo);
+    for (int k = 0; k < Q; ++k) {
+        // right x = w/2+1+d: (x-1, x, x+1) = distances (d-1, d, d+1)
+        nr[k] = heat_f(k == 0 ? inR : vr[k - 1], vr[k], k == Q - 1 ? out.y : vr[k + 1], fo);
+        // left x = w/2-d: (x-1, x, x+1) = distances (d+1, d, d-1)
+        nl[k] = heat_f(k == Q - 1 ? out.x : vl[k + 1], vl[k], k == 0 ? inL : vl[k - 1], fo);
     }
 #pragma unroll
-    for (int k = 0; k < P; ++k) v[k] = nv[k];
+    for (int k = 0; k < Q; ++k) {
+        vl[k] = nl[k];
+        vr[k] = nr[k];
+    }
 }
 
-template <int P>
-__device__ __forceinline__ void insert_left(const TileCtx<P>& c, double (&v)[P], int r, int lo) {
-    const int base = 2 * (r - 1) - (lo - 1) + c.my_lo;
+// Expanding level r: distances r-1 and r from the rings (left value of
+// distance e at ring index 2(r-1) + r - e, right at 2(r-1) + e - (r-1)).
+// Distances beyond r are outside the dependency cone and take any value, so a
+// one-sided predicate suffices.
+template <int Q>
+__device__ __forceinline__ void finsert(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r) {
+    const int d0 = c.s * Q;
 #pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (c.my_lo + k <= lo) v[k] = c.einR[(base + k) & kRingMask];
-}
-template <int P>
-__device__ __forceinline__ void insert_right(const TileCtx<P>& c, double (&v)[P], int r, int hi) {
-    const int base = 2 * (r - 1) - (hi - 1) + c.my_lo;
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (c.my_lo + k >= hi - 1) v[k] = c.einL[(base + k) & kRingMask];
-}
-// (`live` only predicates the stores: control flow must stay warp-uniform
-// because the segment loops contain barriers.)
-template <int P>
-__device__ __forceinline__ void export_left(const TileCtx<P>& c, const double (&v)[P], int d, int lo, double* oL,
-                                            bool live) {
-    double* dst = oL + 2 * d - lo + c.my_lo;
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (live && (unsigned)(c.my_lo + k - lo) < 2u) dst[k] = v[k];
-}
-template <int P>
-__device__ __forceinline__ void export_right(const TileCtx<P>& c, const double (&v)[P], int d, int hi, double* oR,
-                                             bool live) {
-    double* dst = oR + 2 * d - (hi - 2) + c.my_lo;
-#pragma unroll
-    for (int k = 0; k < P; ++k)
-        if (live && (unsigned)(c.my_lo + k - (hi - 2)) < 2u) dst[k] = v[k];
+    for (int k = 0; k < Q; ++k) {
+        if (d0 + k >= r - 1) {
+            vl[k] = c.ringR[ridx(3 * r - 2 - d0 - k, c.g, c.G)];
+            vr[k] = c.ringL[ridx(r - 1 + d0 + k, c.g, c.G)];
+        }
+    }
 }
 
-// Expanding levels [r0, r1): span [w/2+1-r, w/2+1+r).
-template <int P, bool IL, bool IR, bool CP, class Feed>
-__device__ __forceinline__ void expand_seg(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
-                                           Feed& feed) {
+// Contracting exports of level m+d (edge layout [level][2]).
+template <int Q>
+__device__ __forceinline__ void fexport(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int d,
+                                        double* oL, double* oR, bool live) {
+    const int d0 = c.s * Q, e1 = c.m - 1 - d, e2 = c.m - 2 - d;
+#pragma unroll
+    for (int k = 0; k < Q; ++k) {
+        if (live && d0 + k == e1) {
+            oL[2 * d] = vl[k];
+            oR[2 * d + 1] = vr[k];
+        }
+        if (live && d0 + k == e2) {
+            oL[2 * d + 1] = vl[k];
+            oR[2 * d] = vr[k];
+        }
+    }
+    if (live && e2 < 0 && c.s == 0) { // last level: (x=m, m+1) = (left 0, right 0)
+        oL[2 * d + 1] = vr[0];
+        oR[2 * d] = vl[0];
+    }
+}
+
+// Level loops in segments with compile-time roles (control flow warp-uniform:
+// the loops contain barriers; `live` only predicates stores).
+template <int Q, bool INS, bool CP, class Feed>
+__device__ __forceinline__ void fexpand_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
+                                            double fo, Feed& feed) {
     for (int r = r0; r < r1; ++r) {
-        const int lo = c.w / 2 + 1 - r, hi = c.w / 2 + 1 + r;
-        if (IL) insert_left(c, v, r, lo);
-        if (IR) insert_right(c, v, r, hi);
-        if (IL || IR || CP) publish(c, v, r);
+        if (INS) finsert(c, vl, vr, r);
+        if (INS || CP) fpublish(c, vl, vr, r);
         feed(r);
         S1D_LEVEL_BARRIER();
-        if (CP) compute_span(c, v, r, fo);
+        if (CP) fcompute(c, vl, vr, r, fo);
     }
 }
 
-template <int P, class Feed>
-__device__ __forceinline__ void expand_levels(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
-                                              Feed& feed) {
-    const int h2 = c.w / 2;
-    // role ranges (inclusive) for this warp's x in [wlo, whi]
-    const int rc = max(h2 + 1 - c.whi, c.wlo - h2);  // computes from rc on
-    const int aL = h2 - c.whi, bL = h2 + 1 - c.wlo;  // left inserts
-    const int aR = c.wlo - h2 - 1, bR = c.whi - h2;  // right inserts
-    int bnd[6] = {rc, aL, bL + 1, aR, bR + 1, r1};
-#pragma unroll
-    for (int i = 1; i < 6; ++i) // insertion sort (6 warp-uniform ints)
-        for (int j = i; j > 0 && bnd[j - 1] > bnd[j]; --j) {
-            const int tmp = bnd[j];
-            bnd[j] = bnd[j - 1];
-            bnd[j - 1] = tmp;
-        }
-    int r = r0;
-#pragma unroll 1
-    for (int i = 0; i < 6 && r < r1; ++i) {
-        const int e = min(max(bnd[i], r), r1);
-        if (e <= r) continue;
-        const int f = ((r >= aL && r <= bL) ? 4 : 0) | ((r >= aR && r <= bR) ? 2 : 0) | (r >= rc ? 1 : 0);
-        switch (f) {
-        case 0: expand_seg<P, false, false, false>(c, v, r, e, fo, feed); break;
-        case 1: expand_seg<P, false, false, true>(c, v, r, e, fo, feed); break;
-        case 2: expand_seg<P, false, true, false>(c, v, r, e, fo, feed); break;
-        case 3: expand_seg<P, false, true, true>(c, v, r, e, fo, feed); break;
-        case 4: expand_seg<P, true, false, false>(c, v, r, e, fo, feed); break;
-        case 5: expand_seg<P, true, false, true>(c, v, r, e, fo, feed); break;
-        case 6: expand_seg<P, true, true, false>(c, v, r, e, fo, feed); break;
-        default: expand_seg<P, true, true, true>(c, v, r, e, fo, feed); break;
-        }
-        r = e;
-    }
+// Expanding levels [r0, r1), span distances [0, r): idle below sa*Q, insert
+// while r in [sa*Q, (sb+1)*Q], compute from sa*Q + 1.
+template <int Q, class Feed>
+__device__ __forceinline__ void fexpand(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
+                                        double fo, Feed& feed) {
+    const int a = c.sa * Q, bi = (c.sb + 1) * Q + 1;
+    const int e0 = min(max(a, r0), r1), e1 = min(max(a + 1, r0), r1), e2 = min(max(bi, r0), r1);
+    fexpand_seg<Q, false, false>(c, vl, vr, r0, e0, fo, feed);
+    fexpand_seg<Q, true, false>(c, vl, vr, e0, e1, fo, feed);
+    fexpand_seg<Q, true, true>(c, vl, vr, e1, e2, fo, feed);
+    fexpand_seg<Q, false, true>(c, vl, vr, e2, r1, fo, feed);
 }
 
-// Contracting levels [r0, r1): d = r-m, span [1+d, 1+w-d).
-template <int P, bool PB, bool CP, bool EL, bool ER>
-__device__ __forceinline__ void contract_seg(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
-                                             double* oL, double* oR, bool live) {
+template <int Q, bool PB, bool CP, bool EX>
+__device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
+                                              double fo, double* oL, double* oR, bool live) {
     for (int r = r0; r < r1; ++r) {
-        const int d = r - c.m, lo = 1 + d, hi = 1 + c.w - d;
-        if (PB) publish(c, v, r);
+        if (PB) fpublish(c, vl, vr, r);
         S1D_LEVEL_BARRIER();
-        if (CP) compute_span(c, v, r, fo);
-        if (EL) export_left(c, v, d, lo, oL, live);
-        if (ER) export_right(c, v, d, hi, oR, live);
+        if (CP) fcompute(c, vl, vr, r, fo);
+        if (EX) fexport(c, vl, vr, r - c.m, oL, oR, live);
     }
 }
 
-template <int P>
-__device__ __forceinline__ void contract_levels(const TileCtx<P>& c, double (&v)[P], int r0, int r1, double fo,
-                                                double* oL, double* oR, bool live) {
-    const int m = c.m, w = c.w;
-    const int rce = m + min(c.whi - 1, w - c.wlo);      // computes while r <= rce
-    const int rpe = m + min(c.whi, w + 1 - c.wlo);      // publishes while r <= rpe
-    const int aL = m + c.wlo - 2, bL = m + c.whi - 1;   // left exports
-    const int aR = m + w - 1 - c.whi, bR = m + w - c.wlo; // right exports
-    int bnd[7] = {rce + 1, rpe + 1, aL, bL + 1, aR, bR + 1, r1};
-#pragma unroll
-    for (int i = 1; i < 7; ++i)
-        for (int j = i; j > 0 && bnd[j - 1] > bnd[j]; --j) {
-            const int tmp = bnd[j];
-            bnd[j] = bnd[j - 1];
-            bnd[j - 1] = tmp;
-        }
-    int r = r0;
-#pragma unroll 1
-    for (int i = 0; i < 7 && r < r1; ++i) {
-        const int e = min(max(bnd[i], r), r1);
-        if (e <= r) continue;
-        const bool pb = r <= rpe, cp = r <= rce;
-        const bool el = r >= aL && r <= bL, er = r >= aR && r <= bR; // warp-uniform
-        if (!pb) contract_seg<P, false, false, false, false>(c, v, r, e, fo, oL, oR, live);
-        else if (!cp) contract_seg<P, true, false, false, false>(c, v, r, e, fo, oL, oR, live);
-        else if (el && er) contract_seg<P, true, true, true, true>(c, v, r, e, fo, oL, oR, live);
-        else if (el) contract_seg<P, true, true, true, false>(c, v, r, e, fo, oL, oR, live);
-        else if (er) contract_seg<P, true, true, false, true>(c, v, r, e, fo, oL, oR, live);
-        else contract_seg<P, true, true, false, false>(c, v, r, e, fo, oL, oR, live);
-        r = e;
-    }
+// Contracting levels [r0, r1), r = m+d, span distances [0, m-d): compute
+// while r <= 2m-1-sa*Q, export from 2m-1-(sb+1)*Q on, publish one level longer.
+template <int Q>
+__device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
+                                          double fo, double* oL, double* oR, bool live) {
+    const int rce = 2 * c.m - 1 - c.sa * Q, ae = 2 * c.m - 1 - (c.sb + 1) * Q;
+    const int e0 = min(max(ae, r0), r1), e1 = min(max(rce + 1, r0), r1), e2 = min(max(rce + 2, r0), r1);
+    fcontract_seg<Q, true, true, false>(c, vl, vr, r0, e0, fo, oL, oR, live);
+    fcontract_seg<Q, true, true, true>(c, vl, vr, e0, e1, fo, oL, oR, live);
+    fcontract_seg<Q, true, false, false>(c, vl, vr, e1, e2, fo, oL, oR, live);
+    fcontract_seg<Q, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
 }
 
-template <int P, int KIND, int MAXT>
+// Shared memory (doubles): exchange 8*(tt+2)*G, then max(ring 4*kRing*G for
+// Diamond/Down, staging G*(w+1) for Up/Down; the Down staging reuses the ring).
+__host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P, int G) {
+    const std::size_t tt = (std::size_t)(w / P);
+    const std::size_t ring = kind != kUp ? 4 * (std::size_t)kRing * G : 0;
+    const std::size_t stage = kind != kDiamond ? (std::size_t)G * (w + 1) : 0;
+    return 8 * (tt + 2) * G + (ring > stage ? ring : stage);
+}
+
+template <int Q, int KIND, int MAXT>
 __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G) {
-    extern __shared__ double sm[];
+    extern __shared__ __align__(16) double sm[];
     const int w = a.w, m = a.m;
-    const int tt = w / P;                 // threads per tile
+    const int tt = m / Q; // slots per tile
+    const int nt = tt * G;
     const int t = threadIdx.x;
-    const int g = t / tt;                 // tile within the CTA
-    const int b = a.b0 + blockIdx.x * G + g; // tile index in the shard
-    const bool live = b < (a.b1 < 0 ? a.nb : a.b1);
+    const int s = t / G, g = t - s * G;
+    const int bfirst = a.b0 + blockIdx.x * G; // first tile of this CTA
+    const int bend = a.b1 < 0 ? a.nb : a.b1;
+    const int ntiles = min(G, bend - bfirst);
+    const int b = bfirst + g;
+    const bool live = g < ntiles;
     const double fo = a.fourier;
 
-    TileCtx<P> c;
-    c.w = w;
+    Fold<Q> c;
     c.m = m;
-    c.tt = tt;
-    c.lt = t - g * tt;
-    c.my_lo = 1 + c.lt * P;
-    c.xs = G * (tt + 2);
-    c.XL = sm;
-    c.XF = sm + 2 * c.xs;
-    c.slot = g * (tt + 2) + c.lt + 1;
-    double* einR = sm + 4 * c.xs + (std::size_t)g * tile_edge_stride(w);
-    double* einL = einR + 2 * kRing;
-    c.einR = einR;
-    c.einL = einL;
+    c.G = G;
+    c.s = s;
+    c.g = g;
+    c.xs = (tt + 2) * G;
+    c.F = reinterpret_cast<double2*>(sm);
+    c.Lst = c.F + 2 * c.xs;
+    double* const ringR = sm + 8 * c.xs; // [2*kRing][G]
+    double* const ringL = ringR + 2 * kRing * G;
+    double* const stage = ringR;         // Up/Down [G][w+1]
+    c.ringR = ringR;
+    c.ringL = ringL;
     {
-        // Warp x-range (superset when a warp spans several tiles).
         const unsigned full = __activemask();
-        c.wlo = __reduce_min_sync(full, c.my_lo);
-        c.whi = __reduce_max_sync(full, c.my_lo + P - 1);
+        c.sa = (int)__reduce_min_sync(full, (unsigned)s);
+        c.sb = (int)__reduce_max_sync(full, (unsigned)s);
     }
-
-    const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
-    double v[P];
+    const int ws = w + 1;
+    double vl[Q], vr[Q];
 #pragma unroll
-    for (int k = 0; k < P; ++k) v[k] = 0.0;
+    for (int k = 0; k < Q; ++k) vl[k] = vr[k] = 0.0;
 
-    if (KIND == kUp) {
-        if (live) {
-            const double* src = a.state_in + (std::size_t)b * w + (std::size_t)c.lt * P;
+    if (KIND == kUp) { // coalesced staging of the CTA's ntiles*w contiguous points
+        const double* src = a.state_in + (std::size_t)bfirst * w;
+        for (int j = t; j < ntiles * w; j += nt) {
+            const int gg = j / w;
+            stage[gg * ws + (j - gg * w)] = src[j];
+        }
+        __syncthreads();
+        const double* my = stage + g * ws; // core x-1: left d at m-1-d, right d at m+d
 #pragma unroll
-            for (int k = 0; k < P; ++k) v[k] = src[k];
+        for (int k = 0; k < Q; ++k) {
+            vl[k] = my[m - 1 - (s * Q + k)];
+            vr[k] = my[m + s * Q + k];
         }
     }
-    // Edge streaming (Diamond/Down). The tile's threads load levels
-    // 1..min(m, kRing) cooperatively; for longer tiles thread lt == 0 then
-    // queues level r+kRing-1 into the slot freed by level r-1 (cp.async, one
-    // group per level) and waits so that level r+1 has landed before barrier r.
+
+    // Edge sources: left producer's R edges and right producer's L edges.
+    auto srcR = [&](int bb) -> const double* {
+        if (a.seam) return a.in_R + (std::size_t)bb * w;
+        return bb > 0 ? a.in_R + (std::size_t)(bb - 1) * w : a.peer_R;
+    };
+    auto srcL = [&](int bb) -> const double* {
+        if (a.seam) return bb + 1 < a.nb ? a.in_L + (std::size_t)(bb + 1) * w : a.peer_L;
+        return a.in_L + (std::size_t)bb * w;
+    };
     const double* pR = nullptr;
     const double* pL = nullptr;
-    const bool feeder = live && c.lt == 0 && KIND != kUp && m > kRing;
+    const bool feeder = live && s == 0 && KIND != kUp && m > kRing;
     if (KIND != kUp) {
         if (live) {
-            if (a.seam) {
-                pR = a.in_R + (std::size_t)b * w;
-                pL = (b + 1 < a.nb) ? a.in_L + (std::size_t)(b + 1) * w : a.peer_L;
-            } else {
-                pR = (b > 0) ? a.in_R + (std::size_t)(b - 1) * w : a.peer_R;
-                pL = a.in_L + (std::size_t)b * w;
-            }
-            const int n0 = 2 * (m < kRing ? m : kRing);
-            for (int i = c.lt; i < n0; i += tt) {
-                einR[i] = pR[i];
-                einL[i] = pL[i];
-            }
+            pR = srcR(b);
+            pL = srcL(b);
+        }
+        // Levels 1..min(m, kRing), whole CTA, coalesced per tile.
+        const int n0 = 2 * (m < kRing ? m : kRing);
+        for (int j = t; j < ntiles * n0; j += nt) {
+            const int gg = j / n0, i = j - gg * n0;
+            ringR[ridx(i, gg, G)] = srcR(bfirst + gg)[i];
+            ringL[ridx(i, gg, G)] = srcL(bfirst + gg)[i];
         }
         __syncthreads();
     }
+    // Longer tiles: slot-0 threads queue level r+kRing-1 into the ring entries
+    // freed by level r-1 (cp.async, one group per level) and wait so that
+    // level r+1 has landed before barrier r.
     auto feed = [&](int r) {
         if (feeder) {
             const int q = r + kRing - 2; // 0-based index of level r+kRing-1
             if (q < m) {
-                cp_async16(einR + ((2 * q) & kRingMask), pR + 2 * q);
-                cp_async16(einL + ((2 * q) & kRingMask), pL + 2 * q);
+                cp_async8(ringR + ridx(2 * q, g, G), pR + 2 * q);
+                cp_async8(ringR + ridx(2 * q + 1, g, G), pR + 2 * q + 1);
+                cp_async8(ringL + ridx(2 * q, g, G), pL + 2 * q);
+                cp_async8(ringL + ridx(2 * q + 1, g, G), pL + 2 * q + 1);
             }
             cp_async_commit();
             cp_async_wait<kRing - 2>();
@@ -411,31 +438,38 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
     double* oR = a.out_R + (std::size_t)b * w;
 
     if (KIND != kUp) {
-        // Expanding half, levels 1..m-1 (span [w/2+1-r, w/2+1+r)), then m.
-        expand_levels(c, v, 1, m, fo, feed);
-        {
-            const int r = m, lo = 1, hi = w + 1;
-            insert_level(c, v, r, lo, hi);
-            publish(c, v, r);
-            const int par = (r & 1) * c.xs;
-            const int base = g * (tt + 2);
-            if (c.lt == 0) c.XL[par + base] = einR[(2 * (m - 1)) & kRingMask];               // x = 0
-            if (c.lt == tt - 1) c.XF[par + base + tt + 1] = einL[(2 * (m - 1) + 1) & kRingMask]; // x = w+1
+        fexpand(c, vl, vr, 1, m, fo, feed);
+        { // level m: full span; the halo pair (x = 0, w+1) is distance m
+            const int r = m;
+            finsert(c, vl, vr, r);
+            fpublish(c, vl, vr, r);
+            if (s == tt - 1)
+                c.F[(r & 1) * c.xs + (tt + 1) * G + g] =
+                    make_double2(ringR[ridx(2 * (m - 1), g, G)], ringL[ridx(2 * (m - 1) + 1, g, G)]);
             __syncthreads();
-            compute_level(c, v, r, lo, hi, fo);
+            fcompute(c, vl, vr, r, fo);
         }
     }
     if (KIND != kDown) {
-        // Contracting half, levels m..2m-1: span [1+d, 1+w-d), d = r-m.
-        if (live) export_level(c, v, 0, 1, w + 1, oL, oR);
-        contract_levels(c, v, m + 1, 2 * m, fo, oL, oR, live);
-    } else if (live) {
-        const std::int64_t g0 = centre - w / 2 + (std::int64_t)c.lt * P;
+        fexport(c, vl, vr, 0, oL, oR, live);
+        fcontract(c, vl, vr, m + 1, 2 * m, fo, oL, oR, live);
+    } else {
+        __syncthreads(); // ring reads done before the staging reuses it
+        double* my = stage + g * ws;
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-            const std::uint64_t gp = (std::uint64_t)(g0 + k);
-            if (gp < a.N) a.state_out[gp] = v[k];
-            else a.state_right[gp - a.N] = v[k];
+        for (int k = 0; k < Q; ++k) {
+            my[m - 1 - (s * Q + k)] = vl[k];
+            my[m + s * Q + k] = vr[k];
+        }
+        __syncthreads();
+        const std::int64_t centre0 = a.seam ? (std::int64_t)(bfirst + 1) * w : (std::int64_t)bfirst * w + w / 2;
+        const std::int64_t p0 = centre0 - w / 2; // shard position of the CTA's first core point
+        for (int j = t; j < ntiles * w; j += nt) {
+            const int gg = j / w;
+            const double val = stage[gg * ws + (j - gg * w)];
+            const std::uint64_t gp = (std::uint64_t)(p0 + j);
+            if (gp < a.N) a.state_out[gp] = val;
+            else a.state_right[gp - a.N] = val;
         }
     }
 }
@@ -568,13 +602,14 @@ int tiles_per_cta(int w, int p) {
 
 template <int P, int MAXT = 256>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
+    static_assert(P % 2 == 0, "the folded layout holds P/2 distance pairs per thread");
     const int tt = a.w / P;
     const int G = tiles_per_cta(a.w, P);
     const int nt = G * tt;
-    const size_t smem = sizeof(double) * (4 * (size_t)G * (tt + 2) + (size_t)G * tile_edge_stride(a.w));
-    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P, kUp, MAXT>
-                                     : kind == kDiamond ? heat_tile_kernel<P, kDiamond, MAXT>
-                                                        : heat_tile_kernel<P, kDown, MAXT>;
+    const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
+    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT>
+                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT>
+                                                        : heat_tile_kernel<P / 2, kDown, MAXT>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -591,15 +626,18 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
 int heat_points_per_thread(int w) {
     if (const char* e = std::getenv("S1D_HEAT_P")) {
         const int p = std::atoi(e);
-        if ((p == 1 || p == 2 || p == 4 || p == 8 || p == 16) && w % p == 0 && w / p <= 256) return p;
+        if ((p == 2 || p == 4 || p == 8 || p == 16) && w % p == 0 && w / p <= 256) return p;
     }
-    // 256 threads per tile for wide tiles (P = w/256); P = 4 for narrow ones
-    // (several tiles per CTA); always P | w, 2 <= P <= 16, w/P <= 256.
+    // Folded layout: P even (P/2 distance pairs per thread). Measured on B200
+    // (n = 2^27): P = 8 is fastest from w = 64 up, P = 4 at w = 32; wide tiles
+    // double P until w/P <= 256 threads. Always P | w, w/P <= 256 except for
+    // w = 2 mod 4 (P = 2, up to 1024 threads).
     int p = 2;
-    if (w % 4 == 0) p = 4;
+    if (w % 8 == 0 && w >= 64) p = 8;
+    else if (w % 4 == 0) p = 4;
     while (w / p > 256 && w % (2 * p) == 0 && p < 16) p *= 2;
     if (w / p > 1024) return -1; // no valid decomposition (caller reports it)
-    return p;                    // w/p in (256, 1024] only for w = 2 mod 4 (P = 2, wide CTA)
+    return p;
 }
 
 cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st) {
@@ -647,7 +685,6 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     }
     if (a.w / a.p > 256) return a.p == 2 ? launch_tile_p<2, 1024>(kind, a, st) : cudaErrorInvalidValue;
     switch (a.p) {
-    case 1: return launch_tile_p<1>(kind, a, st);
     case 2: return launch_tile_p<2>(kind, a, st);
     case 4: return launch_tile_p<4>(kind, a, st);
     case 8: return launch_tile_p<8>(kind, a, st);
