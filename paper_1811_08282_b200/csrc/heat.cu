@@ -70,7 +70,10 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
 // level per side) filled with cp.async kRing-2 levels ahead of use, so shared
 // memory per tile is O(1) in w. The ring index of (level r, x) is affine in x
 // and wrapped with a mask.
-constexpr int kRing = 32;             // levels held per side (power of two)
+#ifndef S1D_HEAT_RING
+#define S1D_HEAT_RING 16
+#endif
+constexpr int kRing = S1D_HEAT_RING;  // levels held per side (power of two)
 constexpr int kRingMask = 2 * kRing - 1;
 __host__ __device__ inline int tile_edge_stride(int) { return 4 * kRing; }
 
@@ -194,9 +197,19 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
 
-// Ring element i (edge value index 2*level+j, wrapped) of tile g; G is a power of two.
-__device__ __forceinline__ int ridx(int i, int g, int G) {
-    i &= kRingMask;
+// Production rings hold min(kRing, pow2ceil(m)) levels (short tiles need no
+// more), so narrow tiles keep shared memory — and occupancy — small.
+__host__ __device__ inline int ring_levels(int m) {
+    if (m >= kRing) return kRing;
+    int l = 1;
+    while (l < m) l *= 2;
+    return l;
+}
+
+// Ring element i (edge value index 2*level+j, wrapped by mask = 2*levels-1) of
+// tile g; G is a power of two.
+__device__ __forceinline__ int ridx(int i, int mask, int g, int G) {
+    i &= mask;
     return i * G + (g ^ (i & (G - 1)));
 }
 
@@ -207,6 +220,7 @@ struct Fold {
     double2* F;          // [2][(tt+2)G]: (vl[0], vr[0]) of slot s at (s+1)G+g
     double2* Lst;        // [2][(tt+2)G]: (vl[Q-1], vr[Q-1]) of slot s at (s+1)G+g
     int xs;              // parity stride (double2 elements)
+    int rmask;           // ring index mask
     const double* ringR; // left producer's R edges
     const double* ringL; // right producer's L edges
 };
@@ -250,8 +264,8 @@ __device__ __forceinline__ void finsert(const Fold<Q>& c, double (&vl)[Q], doubl
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         if (d0 + k >= r - 1) {
-            vl[k] = c.ringR[ridx(3 * r - 2 - d0 - k, c.g, c.G)];
-            vr[k] = c.ringL[ridx(r - 1 + d0 + k, c.g, c.G)];
+            vl[k] = c.ringR[ridx(3 * r - 2 - d0 - k, c.rmask, c.g, c.G)];
+            vr[k] = c.ringL[ridx(r - 1 + d0 + k, c.rmask, c.g, c.G)];
         }
     }
 }
@@ -329,17 +343,19 @@ __device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], dou
     fcontract_seg<Q, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
 }
 
-// Shared memory (doubles): exchange 8*(tt+2)*G, then max(ring 4*kRing*G for
+// Shared memory (doubles): exchange 8*(tt+2)*G, then max(ring 4*levels*G for
 // Diamond/Down, staging G*(w+1) for Up/Down; the Down staging reuses the ring).
 __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P, int G) {
     const std::size_t tt = (std::size_t)(w / P);
-    const std::size_t ring = kind != kUp ? 4 * (std::size_t)kRing * G : 0;
+    const std::size_t ring = kind != kUp ? 4 * (std::size_t)ring_levels(w / 2) * G : 0;
     const std::size_t stage = kind != kDiamond ? (std::size_t)G * (w + 1) : 0;
     return 8 * (tt + 2) * G + (ring > stage ? ring : stage);
 }
 
-template <int Q, int KIND, int MAXT>
-__global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G) {
+// MINB > 1 caps registers for occupancy (measured: +2-4% for w >= 256 at
+// P = 8; slower for narrow tiles, whose shared memory already limits it).
+template <int Q, int KIND, int MAXT, int MINB>
+__global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
     const int w = a.w, m = a.m;
     const int tt = m / Q; // slots per tile
@@ -361,8 +377,11 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
     c.xs = (tt + 2) * G;
     c.F = reinterpret_cast<double2*>(sm);
     c.Lst = c.F + 2 * c.xs;
-    double* const ringR = sm + 8 * c.xs; // [2*kRing][G]
-    double* const ringL = ringR + 2 * kRing * G;
+    const int rl = ring_levels(m);
+    const int rmask = 2 * rl - 1;
+    c.rmask = rmask;
+    double* const ringR = sm + 8 * c.xs; // [2*rl][G]
+    double* const ringL = ringR + 2 * rl * G;
     double* const stage = ringR;         // Up/Down [G][w+1]
     c.ringR = ringR;
     c.ringL = ringL;
@@ -412,8 +431,8 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
         const int n0 = 2 * (m < kRing ? m : kRing);
         for (int j = t; j < ntiles * n0; j += nt) {
             const int gg = j / n0, i = j - gg * n0;
-            ringR[ridx(i, gg, G)] = srcR(bfirst + gg)[i];
-            ringL[ridx(i, gg, G)] = srcL(bfirst + gg)[i];
+            ringR[ridx(i, rmask, gg, G)] = srcR(bfirst + gg)[i];
+            ringL[ridx(i, rmask, gg, G)] = srcL(bfirst + gg)[i];
         }
         __syncthreads();
     }
@@ -424,10 +443,10 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
         if (feeder) {
             const int q = r + kRing - 2; // 0-based index of level r+kRing-1
             if (q < m) {
-                cp_async8(ringR + ridx(2 * q, g, G), pR + 2 * q);
-                cp_async8(ringR + ridx(2 * q + 1, g, G), pR + 2 * q + 1);
-                cp_async8(ringL + ridx(2 * q, g, G), pL + 2 * q);
-                cp_async8(ringL + ridx(2 * q + 1, g, G), pL + 2 * q + 1);
+                cp_async8(ringR + ridx(2 * q, rmask, g, G), pR + 2 * q);
+                cp_async8(ringR + ridx(2 * q + 1, rmask, g, G), pR + 2 * q + 1);
+                cp_async8(ringL + ridx(2 * q, rmask, g, G), pL + 2 * q);
+                cp_async8(ringL + ridx(2 * q + 1, rmask, g, G), pL + 2 * q + 1);
             }
             cp_async_commit();
             cp_async_wait<kRing - 2>();
@@ -445,7 +464,7 @@ __global__ void __launch_bounds__(MAXT) heat_tile_kernel(const TileArgs a, int G
             fpublish(c, vl, vr, r);
             if (s == tt - 1)
                 c.F[(r & 1) * c.xs + (tt + 1) * G + g] =
-                    make_double2(ringR[ridx(2 * (m - 1), g, G)], ringL[ridx(2 * (m - 1) + 1, g, G)]);
+                    make_double2(ringR[ridx(2 * (m - 1), rmask, g, G)], ringL[ridx(2 * (m - 1) + 1, rmask, g, G)]);
             __syncthreads();
             fcompute(c, vl, vr, r, fo);
         }
@@ -600,16 +619,16 @@ int tiles_per_cta(int w, int p) {
     return G;
 }
 
-template <int P, int MAXT = 256>
+template <int P, int MAXT = 256, int MINB = 1>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     static_assert(P % 2 == 0, "the folded layout holds P/2 distance pairs per thread");
     const int tt = a.w / P;
     const int G = tiles_per_cta(a.w, P);
     const int nt = G * tt;
     const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
-    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT>
-                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT>
-                                                        : heat_tile_kernel<P / 2, kDown, MAXT>;
+    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT, MINB>
+                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB>
+                                                        : heat_tile_kernel<P / 2, kDown, MAXT, MINB>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -687,7 +706,7 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     switch (a.p) {
     case 2: return launch_tile_p<2>(kind, a, st);
     case 4: return launch_tile_p<4>(kind, a, st);
-    case 8: return launch_tile_p<8>(kind, a, st);
+    case 8: return a.w >= 256 ? launch_tile_p<8, 256, 5>(kind, a, st) : launch_tile_p<8>(kind, a, st);
     case 16: return launch_tile_p<16>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
