@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define S1D_ABI_VERSION 1
+#define S1D_ABI_VERSION 2
 
 /* Status codes. 1..10 map one-to-one onto the reference exception types
  * (inc/errors.hpp:8-47); 20+ are device-side conditions. */
@@ -101,6 +101,8 @@ typedef struct s1d_stats {
     uint64_t exchange_rounds;
     uint64_t kernel_launches;   /* device kernels launched by the stepping loop */
     uint64_t edge_bytes_device; /* bytes read across shard boundaries */
+    double virtual_comm_seconds; /* CommStats::virtual_comm_time: per-rank sum of
+                                    alpha + beta*bytes over rounds (any mode) */
 } s1d_stats;
 
 /* EngineTiming (inc/engine.hpp:12-16). loop_seconds = max over shards of the
@@ -235,6 +237,22 @@ int s1d_power_law_fit(const double* n, const double* t, size_t count, double* A,
 /* best_config (src/perf.cpp:84-97): index of the fastest record (ties: smaller
  * w, then smaller WF), or -status. [host] */
 int64_t s1d_best_config(const s1d_record* recs, size_t n);
+
+/* ---- alpha-beta virtual-time model -------------------------------------- */
+/* The reference's VirtualTime clock for cfg's run (RingTransport
+ * advance_clock/round cost, transport.cpp:73-90, 173-182; advance points
+ * engines_impl.hpp:201-213, 249-321; result engines_impl.hpp:413), replayed
+ * without running the stencil: *virtual_seconds = the final max rank clock
+ * (RunResult.timing.virtual_seconds in virtual mode), *comm_seconds = the
+ * per-rank sum of round costs (CommStats::virtual_comm_time, any mode).
+ * Uses cfg->alpha, beta, compute_cost; cfg is copied and finalized. s1d_run
+ * and s1d_measure report the same values. [host] */
+int s1d_virtual_time(const s1d_config* cfg, double* virtual_seconds, double* comm_seconds, char* err,
+                     size_t errlen);
+/* Measured transport parameters between two devices for the model above:
+ * *alpha = one-way latency (s) of a device-side flag hand-off over NVLink (the
+ * swept round's synchronisation), *beta = s/byte of a 256 MiB peer copy. */
+int s1d_calibrate_transport(int dev_a, int dev_b, double* alpha, double* beta, char* err, size_t errlen);
 
 /* ---- measurement helpers (not part of the reference interface) --------- */
 /* Sustained FP64 DADD/DMUL instruction rate of `device` (ops/s), measured by

@@ -120,7 +120,8 @@ class RefCfg(C.Structure):
 class RefStats(C.Structure):
     _fields_ = [("messages_sent", C.c_ulonglong), ("bytes_sent", C.c_ulonglong),
                 ("exchange_rounds", C.c_ulonglong), ("setup_seconds", C.c_double),
-                ("loop_seconds", C.c_double), ("virtual_seconds", C.c_double)]
+                ("loop_seconds", C.c_double), ("virtual_seconds", C.c_double),
+                ("virtual_comm_time", C.c_double)]
 
 
 class RefMsg(C.Structure):
@@ -228,6 +229,7 @@ class RefResult:
     setup_seconds: float = 0.0
     loop_seconds: float = 0.0
     virtual_seconds: float = 0.0
+    virtual_comm_time: float = 0.0
     log: list = field(default_factory=list)
 
 
@@ -258,7 +260,7 @@ def ref_run(cfg: RefConfig, keep_log: bool = False) -> RefResult:
     if st:
         raise OracleError(st, e.value.decode())
     res = RefResult(out, st_.messages_sent, st_.bytes_sent, st_.exchange_rounds, st_.setup_seconds,
-                    st_.loop_seconds, st_.virtual_seconds)
+                    st_.loop_seconds, st_.virtual_seconds, st_.virtual_comm_time)
     if keep_log:
         res.log = [(m.round, m.source, m.dest, m.tag, m.bytes) for m in logbuf[: min(nlog.value, cap)]]
     return res

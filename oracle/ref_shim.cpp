@@ -51,6 +51,7 @@ struct ref_cfg {
 struct ref_stats {
     unsigned long long messages_sent, bytes_sent, exchange_rounds;
     double setup_seconds, loop_seconds, virtual_seconds;
+    double virtual_comm_time;  // CommStats::virtual_comm_time (transport.hpp:20-30)
 };
 
 struct ref_msg {
@@ -182,6 +183,7 @@ int ref_run(const ref_cfg* c, double* out, size_t cap, ref_stats* st, ref_msg* l
             st->setup_seconds = res.timing.setup_seconds;
             st->loop_seconds = res.timing.loop_seconds;
             st->virtual_seconds = res.timing.virtual_seconds;
+            st->virtual_comm_time = res.stats.virtual_comm_time;
         }
         if (log) {
             const size_t n = res.log.size() < log_cap ? res.log.size() : log_cap;

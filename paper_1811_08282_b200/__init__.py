@@ -16,3 +16,4 @@ from .api import (  # noqa: F401
     FitResult, TimingRecord, best_config, csv_header, csv_row, emit_csv, flattening_speedup, measure, power_law_fit,
     read_csv, speedup)
 from .api import DebugResult, RunOptions, run_debug  # noqa: F401
+from .api import calibrate_transport, virtual_time  # noqa: F401

@@ -29,7 +29,8 @@ class s1d_config(C.Structure):
 
 class s1d_stats(C.Structure):
     _fields_ = [("messages_sent", C.c_uint64), ("bytes_sent", C.c_uint64), ("exchange_rounds", C.c_uint64),
-                ("kernel_launches", C.c_uint64), ("edge_bytes_device", C.c_uint64)]
+                ("kernel_launches", C.c_uint64), ("edge_bytes_device", C.c_uint64),
+                ("virtual_comm_seconds", C.c_double)]
 
 
 class s1d_timing(C.Structure):
@@ -89,6 +90,8 @@ SIGNATURES = {
                             C.POINTER(s1d_timing)]),
     "s1d_last_error": (C.c_char_p, [C.c_void_p]),
     "s1d_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)] + _E),
+    "s1d_virtual_time": (C.c_int, [C.POINTER(s1d_config), _dp, _dp] + _E),
+    "s1d_calibrate_transport": (C.c_int, [C.c_int, C.c_int, _dp, _dp] + _E),
     "s1d_measure": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_record)] + _E),
     "s1d_csv_header": (C.c_char_p, []),
     "s1d_csv_row": (C.c_int64, [C.POINTER(s1d_record), C.c_char_p, C.c_size_t]),

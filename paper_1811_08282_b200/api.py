@@ -23,7 +23,7 @@ from __future__ import annotations
 import ctypes as C
 import enum
 from dataclasses import dataclass, field
-from typing import List, Optional
+from typing import List, Optional, Tuple
 
 import numpy as np
 
@@ -394,6 +394,7 @@ class CommStats:
     kernel_launches: int = 0
     edge_bytes_device: int = 0
     setup_seconds: float = 0.0
+    virtual_comm_time: float = 0.0  # CommStats::virtual_comm_time (transport.hpp:20-30)
 
 
 @dataclass
@@ -419,7 +420,7 @@ class RunResult:
 
 def _stats(s: _capi.s1d_stats, setup: float = 0.0) -> CommStats:
     return CommStats(s.messages_sent, s.bytes_sent, s.exchange_rounds, s.kernel_launches, s.edge_bytes_device,
-                     setup)
+                     setup, s.virtual_comm_seconds)
 
 
 def _timing(t: _capi.s1d_timing) -> EngineTiming:
@@ -585,6 +586,25 @@ class Shard(Solver):
 
     def connect(self, left_blob: bytes, right_blob: bytes) -> None:
         self._chk(lib().s1d_shard_connect(self._h, left_blob, right_blob))
+
+
+def virtual_time(cfg: LaunchConfig) -> Tuple[float, float]:
+    """The reference's alpha-beta virtual clock for `cfg` (host replay, no GPU):
+    (virtual_seconds, virtual_comm_seconds) — what sweep1d::run reports in
+    VirtualTime mode (engines_impl.hpp:413) and CommStats::virtual_comm_time."""
+    v, c = C.c_double(), C.c_double()
+    e = _errbuf()
+    _check(lib().s1d_virtual_time(C.byref(cfg.to_c()), C.byref(v), C.byref(c), e, 1024), e)
+    return v.value, c.value
+
+
+def calibrate_transport(dev_a: int = 0, dev_b: int = 1, compute_cost: float = 1e-8) -> TransportParams:
+    """Measured NVLink alpha (one-way device flag hand-off latency, s) and beta
+    (s/byte of a large peer copy) between two devices, as TransportParams."""
+    a, b = C.c_double(), C.c_double()
+    e = _errbuf()
+    _check(lib().s1d_calibrate_transport(dev_a, dev_b, C.byref(a), C.byref(b), e, 1024), e)
+    return TransportParams(a.value, b.value, compute_cost)
 
 
 def measure_fp64_peak(device: int = 0) -> float:

@@ -718,11 +718,16 @@ struct Solver {
         if (Rn > 1)
             stats.edge_bytes_device += static_cast<std::uint64_t>(pad) * locals.size() * 2 * sizeof(double) *
                                        static_cast<std::uint64_t>(spec.h) * static_cast<std::uint64_t>(spec.rec);
+        {
+            double comm = 0.0;
+            const double vclock = virtual_clock(cfg, &comm);
+            stats.virtual_comm_seconds = comm;
+            if (timing_out) timing_out->virtual_seconds = cfg.mode == S1D_VIRTUAL ? vclock : 0.0;
+        }
         if (stats_out) *stats_out = stats;
         if (timing_out) {
             timing_out->setup_seconds = setup_seconds;
             timing_out->loop_seconds = worst_ms * 1e-3;
-            timing_out->virtual_seconds = 0.0;
             timing_out->dominant_seconds = dom_ms * 1e-3;
             std::uint64_t pts = 0;
             for (int g : locals) pts += sh(g).N;
@@ -949,6 +954,112 @@ int64_t s1d_cycle_advance(uint64_t w, uint64_t h, char* err, size_t errlen) {
     return st == S1D_OK ? static_cast<int64_t>(m) : -st;
 }
 
+int s1d_virtual_time(const s1d_config* cfg, double* virtual_seconds, double* comm_seconds, char* err,
+                     size_t errlen) {
+    return guarded(err, errlen, [&] {
+        s1d_config c = *cfg;
+        s1d::finalize(c, true);
+        double comm = 0.0;
+        const double v = s1d::virtual_clock(c, &comm);
+        if (virtual_seconds) *virtual_seconds = v;
+        if (comm_seconds) *comm_seconds = comm;
+    });
+}
+
+int s1d_calibrate_transport(int dev_a, int dev_b, double* alpha, double* beta, char* err, size_t errlen) {
+    using s1d::CudaError;
+    return guarded(err, errlen, [&] {
+        int nd = 0;
+        if (cudaGetDeviceCount(&nd) != cudaSuccess || nd == 0) {
+            cudaGetLastError();
+            throw s1d::Error(S1D_NO_DEVICE, "no CUDA device visible");
+        }
+        if (dev_a == dev_b || dev_a < 0 || dev_b < 0 || dev_a >= nd || dev_b >= nd)
+            throw s1d::Error(S1D_INVALID_CONFIG, "calibration needs two distinct visible devices");
+        int ab = 0, ba = 0;
+        S1D_CUDA(cudaDeviceCanAccessPeer(&ab, dev_a, dev_b));
+        S1D_CUDA(cudaDeviceCanAccessPeer(&ba, dev_b, dev_a));
+        if (!ab || !ba) throw s1d::Error(S1D_PEER_UNAVAILABLE, "devices cannot access each other's memory");
+        const int devs[2] = {dev_a, dev_b};
+        cudaStream_t st[2];
+        unsigned* flag[2];
+        int* eflag[2];
+        for (int i = 0; i < 2; ++i) {
+            S1D_CUDA(cudaSetDevice(devs[i]));
+            const cudaError_t pe = cudaDeviceEnablePeerAccess(devs[1 - i], 0);
+            if (pe != cudaSuccess && pe != cudaErrorPeerAccessAlreadyEnabled) S1D_CUDA(pe);
+            cudaGetLastError();
+            S1D_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
+            S1D_CUDA(cudaMalloc(&flag[i], 256));
+            S1D_CUDA(cudaMalloc(&eflag[i], sizeof(int)));
+            S1D_CUDA(cudaMemset(eflag[i], 0, sizeof(int)));
+        }
+        cudaEvent_t e0, e1;
+        S1D_CUDA(cudaSetDevice(dev_a));
+        S1D_CUDA(cudaEventCreate(&e0));
+        S1D_CUDA(cudaEventCreate(&e1));
+        // alpha: one-way latency of a flag hand-off (the swept round's sync).
+        auto pingpong = [&](int iters) {
+            for (int i = 0; i < 2; ++i) {
+                S1D_CUDA(cudaSetDevice(devs[i]));
+                S1D_CUDA(cudaMemset(flag[i], 0, 256));
+                S1D_CUDA(cudaDeviceSynchronize());
+            }
+            S1D_CUDA(cudaSetDevice(dev_b));
+            S1D_CUDA(s1d::launch_pingpong(flag[1], flag[0], iters, 0, eflag[1], 10000000000ull, st[1]));
+            S1D_CUDA(cudaSetDevice(dev_a));
+            S1D_CUDA(cudaEventRecord(e0, st[0]));
+            S1D_CUDA(s1d::launch_pingpong(flag[0], flag[1], iters, 1, eflag[0], 10000000000ull, st[0]));
+            S1D_CUDA(cudaEventRecord(e1, st[0]));
+            for (int i = 0; i < 2; ++i) {
+                S1D_CUDA(cudaSetDevice(devs[i]));
+                S1D_CUDA(cudaStreamSynchronize(st[i]));
+                int f = 0;
+                S1D_CUDA(cudaMemcpy(&f, eflag[i], sizeof(int), cudaMemcpyDeviceToHost));
+                if (f) throw s1d::Error(S1D_TRANSPORT_ABORTED, "calibration ping-pong timed out");
+            }
+            float ms = 0.0f;
+            S1D_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+            return static_cast<double>(ms) * 1e-3;
+        };
+        pingpong(200);
+        const int n1 = 2000, n2 = 6000;
+        const double t1 = pingpong(n1), t2 = pingpong(n2);
+        const double a = (t2 - t1) / (2.0 * (n2 - n1));
+        // beta: inverse bandwidth of a large peer copy a -> b.
+        const std::size_t bytes = std::size_t(256) << 20;
+        void* src = nullptr;
+        void* dst = nullptr;
+        S1D_CUDA(cudaSetDevice(dev_b));
+        S1D_CUDA(cudaMalloc(&dst, bytes));
+        S1D_CUDA(cudaSetDevice(dev_a));
+        S1D_CUDA(cudaMalloc(&src, bytes));
+        S1D_CUDA(cudaMemset(src, 0, bytes));
+        S1D_CUDA(cudaMemcpyPeerAsync(dst, dev_b, src, dev_a, bytes, st[0]));
+        const int reps = 4;
+        S1D_CUDA(cudaEventRecord(e0, st[0]));
+        for (int i = 0; i < reps; ++i) S1D_CUDA(cudaMemcpyPeerAsync(dst, dev_b, src, dev_a, bytes, st[0]));
+        S1D_CUDA(cudaEventRecord(e1, st[0]));
+        S1D_CUDA(cudaStreamSynchronize(st[0]));
+        float ms = 0.0f;
+        S1D_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+        const double b = static_cast<double>(ms) * 1e-3 / (static_cast<double>(bytes) * reps);
+        S1D_CUDA(cudaFree(src));
+        S1D_CUDA(cudaEventDestroy(e0));
+        S1D_CUDA(cudaEventDestroy(e1));
+        for (int i = 0; i < 2; ++i) {
+            S1D_CUDA(cudaSetDevice(devs[i]));
+            S1D_CUDA(cudaFree(flag[i]));
+            S1D_CUDA(cudaFree(eflag[i]));
+            S1D_CUDA(cudaStreamDestroy(st[i]));
+        }
+        S1D_CUDA(cudaSetDevice(dev_b));
+        S1D_CUDA(cudaFree(dst));
+        if (alpha) *alpha = a;
+        if (beta) *beta = b;
+    });
+}
+
 int64_t s1d_schedule(int kind, uint64_t w, uint64_t h, int64_t* substep, int64_t* lo, int64_t* hi, size_t cap,
                      char* err, size_t errlen) {
     std::vector<s1d::Level> lv;
@@ -998,12 +1109,14 @@ int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen
         out->work_factor = c.work_factor;
         out->ranks = c.ranks;
         out->steps = c.steps;
-        out->avg_us_per_step = c.steps > 0 ? tm.loop_seconds * 1e6 / static_cast<double>(c.steps) : 0.0;
+        // perf.cpp:21-23: virtual mode reports the modelled clock.
+        const double secs = c.mode == S1D_VIRTUAL ? tm.virtual_seconds : tm.loop_seconds;
+        out->avg_us_per_step = c.steps > 0 ? secs * 1e6 / static_cast<double>(c.steps) : 0.0;
         out->setup_us = tm.setup_seconds * 1e6;
         out->messages_sent = st.messages_sent;
         out->bytes_sent = st.bytes_sent;
         out->exchange_rounds = st.exchange_rounds;
-        out->virtual_comm_us = 0.0;
+        out->virtual_comm_us = st.virtual_comm_seconds * 1e6;
     });
 }
 

@@ -58,4 +58,8 @@ struct Level {
 };
 std::vector<Level> schedule(int kind, std::uint64_t w, std::uint64_t h);
 
+// The reference's alpha-beta virtual clock for a finalized config (host_model.cpp):
+// returns the final max rank clock; *comm_seconds = per-rank sum of round costs.
+double virtual_clock(const s1d_config& cfg, double* comm_seconds);
+
 } // namespace s1d

@@ -88,5 +88,7 @@ std::size_t euler_tile_smem_bytes(int flat, int w);
 cudaError_t launch_wait_flags(const unsigned* flags, unsigned seq, int* err, std::uint64_t timeout_ns,
                               cudaStream_t st);
 cudaError_t launch_signal_flags(unsigned* left_slot, unsigned* right_slot, unsigned seq, cudaStream_t st);
+cudaError_t launch_pingpong(const unsigned* mine, unsigned* peer, int iters, int starter, int* err,
+                            std::uint64_t timeout_ns, cudaStream_t st);
 
 } // namespace s1d

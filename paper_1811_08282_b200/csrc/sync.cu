@@ -56,7 +56,33 @@ __global__ void signal_kernel(unsigned* left_flags_slot, unsigned* right_flags_s
     st_release_sys(right_flags_slot, seq);
 }
 
+// Transport calibration (s1d_calibrate_transport): `iters` flag hand-offs
+// between two devices. The starter stores i into the peer's flag and spins
+// until i comes back; the echo spins for i, then stores it back. One-way
+// latency = elapsed / (2 iters). Bounded by `timeout_ns` like wait_kernel.
+__global__ void pingpong_kernel(const unsigned* mine, unsigned* peer, int iters, int starter, int* err,
+                                std::uint64_t timeout_ns) {
+    if (threadIdx.x != 0) return;
+    const std::uint64_t t0 = globaltimer();
+    for (unsigned i = 1; i <= (unsigned)iters; ++i) {
+        if (starter) st_release_sys(peer, i);
+        while ((int)(ld_acquire_sys(mine) - i) < 0) {
+            if (globaltimer() - t0 > timeout_ns) {
+                atomicOr(err, 2);
+                return;
+            }
+        }
+        if (!starter) st_release_sys(peer, i);
+    }
+}
+
 } // namespace
+
+cudaError_t launch_pingpong(const unsigned* mine, unsigned* peer, int iters, int starter, int* err,
+                            std::uint64_t timeout_ns, cudaStream_t st) {
+    pingpong_kernel<<<1, 32, 0, st>>>(mine, peer, iters, starter, err, timeout_ns);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_wait_flags(const unsigned* flags, unsigned seq, int* err, std::uint64_t timeout_ns,
                               cudaStream_t st) {

@@ -3,6 +3,7 @@ declares; compute entry points report NO_DEVICE (never a CPU fallback) here."""
 import ctypes as C
 import os
 import re
+import subprocess
 
 import pytest
 
@@ -29,14 +30,21 @@ def test_library_exports_every_declared_symbol():
 
 def test_version_and_abi():
     lib = _capi.lib()
-    assert lib.s1d_abi_version() == 1
+    assert lib.s1d_abi_version() == 2
     assert b"sm_100a" in lib.s1d_version()
 
 
-def test_struct_sizes_match_header():
-    # s1d_config: 4 ints, 2 u64, 2 ints, i64, 7 doubles, char[64], int, int[7]
-    assert C.sizeof(_capi.s1d_config) == 4 * 4 + 2 * 8 + 2 * 4 + 8 + 7 * 8 + 64 + 4 + 7 * 4
-    assert C.sizeof(_capi.s1d_stats) == 5 * 8
+def test_struct_sizes_match_header(tmp_path):
+    # sizeof/offsetof from the real header (compiled with gcc) == the ctypes mirror
+    names = ["s1d_config", "s1d_stats", "s1d_timing", "s1d_record", "s1d_debug"]
+    src = tmp_path / "probe.c"
+    src.write_text('#include <stdio.h>\n#include "swept1d.h"\nint main(void) {\n' +
+                   "".join(f'  printf("%zu\\n", sizeof({n}));\n' for n in names) + "  return 0;\n}\n")
+    exe = tmp_path / "probe"
+    inc = os.path.join(os.path.dirname(__file__), "..", "include")
+    subprocess.run(["gcc", "-std=c99", "-I", inc, str(src), "-o", str(exe)], check=True)
+    sizes = [int(x) for x in subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split()]
+    assert sizes == [C.sizeof(getattr(_capi, n)) for n in names]
 
 
 @pytest.mark.skipif(_capi.lib().s1d_device_count() > 0, reason="GPU visible")
