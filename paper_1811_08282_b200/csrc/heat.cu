@@ -294,9 +294,13 @@ __device__ __forceinline__ void fexport(const Fold<Q>& c, const double (&vl)[Q],
 
 // Level loops in segments with compile-time roles (control flow warp-uniform:
 // the loops contain barriers; `live` only predicates stores).
-template <int Q, bool INS, bool CP, class Feed>
+// U: unroll of the long compute-only segments (lets the compiler rename the
+// loop-carried registers instead of copying them; measured per width).
+template <int Q, int U, bool INS, bool CP, class Feed>
 __device__ __forceinline__ void fexpand_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                             double fo, Feed& feed) {
+    constexpr int UN = (!INS && CP) ? U : 1;
+#pragma unroll UN
     for (int r = r0; r < r1; ++r) {
         if (INS) finsert(c, vl, vr, r);
         if (INS || CP) fpublish(c, vl, vr, r);
@@ -308,20 +312,22 @@ __device__ __forceinline__ void fexpand_seg(const Fold<Q>& c, double (&vl)[Q], d
 
 // Expanding levels [r0, r1), span distances [0, r): idle below sa*Q, insert
 // while r in [sa*Q, (sb+1)*Q], compute from sa*Q + 1.
-template <int Q, class Feed>
+template <int Q, int U, class Feed>
 __device__ __forceinline__ void fexpand(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                         double fo, Feed& feed) {
     const int a = c.sa * Q, bi = (c.sb + 1) * Q + 1;
     const int e0 = min(max(a, r0), r1), e1 = min(max(a + 1, r0), r1), e2 = min(max(bi, r0), r1);
-    fexpand_seg<Q, false, false>(c, vl, vr, r0, e0, fo, feed);
-    fexpand_seg<Q, true, false>(c, vl, vr, e0, e1, fo, feed);
-    fexpand_seg<Q, true, true>(c, vl, vr, e1, e2, fo, feed);
-    fexpand_seg<Q, false, true>(c, vl, vr, e2, r1, fo, feed);
+    fexpand_seg<Q, U, false, false>(c, vl, vr, r0, e0, fo, feed);
+    fexpand_seg<Q, U, true, false>(c, vl, vr, e0, e1, fo, feed);
+    fexpand_seg<Q, U, true, true>(c, vl, vr, e1, e2, fo, feed);
+    fexpand_seg<Q, U, false, true>(c, vl, vr, e2, r1, fo, feed);
 }
 
-template <int Q, bool PB, bool CP, bool EX>
+template <int Q, int U, bool PB, bool CP, bool EX>
 __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                               double fo, double* oL, double* oR, bool live) {
+    constexpr int UN = (PB && CP && !EX) ? U : 1;
+#pragma unroll UN
     for (int r = r0; r < r1; ++r) {
         if (PB) fpublish(c, vl, vr, r);
         S1D_LEVEL_BARRIER();
@@ -332,15 +338,15 @@ __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q],
 
 // Contracting levels [r0, r1), r = m+d, span distances [0, m-d): compute
 // while r <= 2m-1-sa*Q, export from 2m-1-(sb+1)*Q on, publish one level longer.
-template <int Q>
+template <int Q, int U>
 __device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                           double fo, double* oL, double* oR, bool live) {
     const int rce = 2 * c.m - 1 - c.sa * Q, ae = 2 * c.m - 1 - (c.sb + 1) * Q;
     const int e0 = min(max(ae, r0), r1), e1 = min(max(rce + 1, r0), r1), e2 = min(max(rce + 2, r0), r1);
-    fcontract_seg<Q, true, true, false>(c, vl, vr, r0, e0, fo, oL, oR, live);
-    fcontract_seg<Q, true, true, true>(c, vl, vr, e0, e1, fo, oL, oR, live);
-    fcontract_seg<Q, true, false, false>(c, vl, vr, e1, e2, fo, oL, oR, live);
-    fcontract_seg<Q, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
+    fcontract_seg<Q, U, true, true, false>(c, vl, vr, r0, e0, fo, oL, oR, live);
+    fcontract_seg<Q, U, true, true, true>(c, vl, vr, e0, e1, fo, oL, oR, live);
+    fcontract_seg<Q, U, true, false, false>(c, vl, vr, e1, e2, fo, oL, oR, live);
+    fcontract_seg<Q, U, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
 }
 
 // Shared memory (doubles): exchange 8*(tt+2)*G, then max(ring 4*levels*G for
@@ -354,7 +360,7 @@ __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P,
 
 // MINB > 1 caps registers for occupancy (measured: +2-4% for w >= 256 at
 // P = 8; slower for narrow tiles, whose shared memory already limits it).
-template <int Q, int KIND, int MAXT, int MINB>
+template <int Q, int KIND, int MAXT, int MINB, int U>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
     const int w = a.w, m = a.m;
@@ -457,7 +463,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     double* oR = a.out_R + (std::size_t)b * w;
 
     if (KIND != kUp) {
-        fexpand(c, vl, vr, 1, m, fo, feed);
+        fexpand<Q, U>(c, vl, vr, 1, m, fo, feed);
         { // level m: full span; the halo pair (x = 0, w+1) is distance m
             const int r = m;
             finsert(c, vl, vr, r);
@@ -471,7 +477,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     }
     if (KIND != kDown) {
         fexport(c, vl, vr, 0, oL, oR, live);
-        fcontract(c, vl, vr, m + 1, 2 * m, fo, oL, oR, live);
+        fcontract<Q, U>(c, vl, vr, m + 1, 2 * m, fo, oL, oR, live);
     } else {
         __syncthreads(); // ring reads done before the staging reuses it
         double* my = stage + g * ws;
@@ -619,16 +625,16 @@ int tiles_per_cta(int w, int p) {
     return G;
 }
 
-template <int P, int MAXT = 256, int MINB = 1>
+template <int P, int MAXT = 256, int MINB = 1, int U = 1>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     static_assert(P % 2 == 0, "the folded layout holds P/2 distance pairs per thread");
     const int tt = a.w / P;
     const int G = tiles_per_cta(a.w, P);
     const int nt = G * tt;
     const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
-    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT, MINB>
-                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB>
-                                                        : heat_tile_kernel<P / 2, kDown, MAXT, MINB>;
+    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U>
+                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U>
+                                                        : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -641,6 +647,10 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
 }
 
 } // namespace
+
+#ifndef S1D_HEAT_U2_MINW
+#define S1D_HEAT_U2_MINW 64
+#endif
 
 int heat_points_per_thread(int w) {
     if (const char* e = std::getenv("S1D_HEAT_P")) {
@@ -706,7 +716,10 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     switch (a.p) {
     case 2: return launch_tile_p<2>(kind, a, st);
     case 4: return launch_tile_p<4>(kind, a, st);
-    case 8: return a.w >= 256 ? launch_tile_p<8, 256, 5>(kind, a, st) : launch_tile_p<8>(kind, a, st);
+    case 8: // measured: register cap (5 CTAs/SM) pays from w = 256, unroll 2 from w = 64
+        if (a.w >= 256) return a.w >= S1D_HEAT_U2_MINW ? launch_tile_p<8, 256, 5, 2>(kind, a, st)
+                                                      : launch_tile_p<8, 256, 5>(kind, a, st);
+        return a.w >= S1D_HEAT_U2_MINW ? launch_tile_p<8, 256, 1, 2>(kind, a, st) : launch_tile_p<8>(kind, a, st);
     case 16: return launch_tile_p<16>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
