@@ -358,8 +358,8 @@ __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P,
     return 8 * (tt + 2) * G + (ring > stage ? ring : stage);
 }
 
-// MINB > 1 caps registers for occupancy (measured: +2-4% for w >= 256 at
-// P = 8; slower for narrow tiles, whose shared memory already limits it).
+// MINB > 1 caps registers for occupancy (P = 8: 64 registers, 4 CTAs/SM, no
+// spills; measured +4-10% over the uncapped build).
 template <int Q, int KIND, int MAXT, int MINB, int U>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
@@ -648,10 +648,6 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
 
 } // namespace
 
-#ifndef S1D_HEAT_U2_MINW
-#define S1D_HEAT_U2_MINW 64
-#endif
-
 int heat_points_per_thread(int w) {
     if (const char* e = std::getenv("S1D_HEAT_P")) {
         const int p = std::atoi(e);
@@ -715,11 +711,9 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     if (a.w / a.p > 256) return a.p == 2 ? launch_tile_p<2, 1024>(kind, a, st) : cudaErrorInvalidValue;
     switch (a.p) {
     case 2: return launch_tile_p<2>(kind, a, st);
-    case 4: return launch_tile_p<4>(kind, a, st);
-    case 8: // measured: register cap (5 CTAs/SM) pays from w = 256, unroll 2 from w = 64
-        if (a.w >= 256) return a.w >= S1D_HEAT_U2_MINW ? launch_tile_p<8, 256, 5, 2>(kind, a, st)
-                                                      : launch_tile_p<8, 256, 5>(kind, a, st);
-        return a.w >= S1D_HEAT_U2_MINW ? launch_tile_p<8, 256, 1, 2>(kind, a, st) : launch_tile_p<8>(kind, a, st);
+    case 4: return launch_tile_p<4>(kind, a, st); // (w = 32: caps/unroll measured slower)
+    case 8: // measured (w = 64 .. 2048): 64-register cap (4 CTAs/SM) + unroll 2
+        return a.w >= 64 ? launch_tile_p<8, 256, 4, 2>(kind, a, st) : launch_tile_p<8>(kind, a, st);
     case 16: return launch_tile_p<16>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
