@@ -349,18 +349,30 @@ __device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], dou
     fcontract_seg<Q, U, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
 }
 
-// Shared memory (doubles): exchange 8*(tt+2)*G, then max(ring 4*levels*G for
-// Diamond/Down, staging G*(w+1) for Up/Down; the Down staging reuses the ring).
+#ifndef S1D_HEAT_XPORT_LEVELS
+#define S1D_HEAT_XPORT_LEVELS 32
+#endif
+constexpr int kXportLevels = S1D_HEAT_XPORT_LEVELS; // stage exports for m <= this (w <= 64)
+
+// Shared memory (doubles): exchange 8*(tt+2)*G, then one region reused in turn:
+// ring 4*levels*G (Diamond/Down), state staging G*(w+1) (Up/Down) and, for
+// short tiles, export staging 2*G*(w+1) (Up/Diamond, after the last ring read).
 __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P, int G) {
     const std::size_t tt = (std::size_t)(w / P);
     const std::size_t ring = kind != kUp ? 4 * (std::size_t)ring_levels(w / 2) * G : 0;
     const std::size_t stage = kind != kDiamond ? (std::size_t)G * (w + 1) : 0;
-    return 8 * (tt + 2) * G + (ring > stage ? ring : stage);
+    // short tiles stage their exports ([2][G][w+1]) in the same region
+    const std::size_t xport = kind != kDown && w / 2 <= kXportLevels ? 2 * (std::size_t)G * (w + 1) : 0; // XS builds
+    std::size_t region = ring > stage ? ring : stage;
+    if (xport > region) region = xport;
+    return 8 * (tt + 2) * G + region;
 }
 
 // MINB > 1 caps registers for occupancy (P = 8: 64 registers, 4 CTAs/SM, no
 // spills; measured +4-10% over the uncapped build).
-template <int Q, int KIND, int MAXT, int MINB, int U>
+// XS: short-tile build (m <= kXportLevels): cp.async ring init and staged
+// exports; wide tiles instantiate XS = false (code identical to before).
+template <int Q, int KIND, int MAXT, int MINB, int U, bool XS>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
     const int w = a.w, m = a.m;
@@ -433,12 +445,25 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
             pR = srcR(b);
             pL = srcL(b);
         }
-        // Levels 1..min(m, kRing), whole CTA, coalesced per tile.
+        // Levels 1..min(m, kRing), whole CTA, coalesced per tile. Short tiles
+        // (the whole edge fits the ring) use cp.async so all of a thread's
+        // loads are in flight at once (measured: +10% at w = 32, -2.6% at
+        // w = 1024, where plain loads win).
         const int n0 = 2 * (m < kRing ? m : kRing);
-        for (int j = t; j < ntiles * n0; j += nt) {
-            const int gg = j / n0, i = j - gg * n0;
-            ringR[ridx(i, rmask, gg, G)] = srcR(bfirst + gg)[i];
-            ringL[ridx(i, rmask, gg, G)] = srcL(bfirst + gg)[i];
+        if (XS && m <= kRing) {
+            for (int j = t; j < ntiles * n0; j += nt) {
+                const int gg = j / n0, i = j - gg * n0;
+                cp_async8(ringR + ridx(i, rmask, gg, G), srcR(bfirst + gg) + i);
+                cp_async8(ringL + ridx(i, rmask, gg, G), srcL(bfirst + gg) + i);
+            }
+            cp_async_commit();
+            cp_async_wait<0>();
+        } else {
+            for (int j = t; j < ntiles * n0; j += nt) {
+                const int gg = j / n0, i = j - gg * n0;
+                ringR[ridx(i, rmask, gg, G)] = srcR(bfirst + gg)[i];
+                ringL[ridx(i, rmask, gg, G)] = srcL(bfirst + gg)[i];
+            }
         }
         __syncthreads();
     }
@@ -476,8 +501,28 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         }
     }
     if (KIND != kDown) {
-        fexport(c, vl, vr, 0, oL, oR, live);
-        fcontract<Q, U>(c, vl, vr, m + 1, 2 * m, fo, oL, oR, live);
+        // Short tiles (m <= kXportLevels) stage their exports in the freed ring /
+        // staging region and write the CTA's contiguous edge block coalesced at
+        // the end (lanes hold different tiles, so direct stores would be 8-byte
+        // scatters at stride w; measured +25% at w = 32, +10% at w = 64).
+        const bool sx = XS; // launcher guarantees m <= kXportLevels
+        double* const xL = ringR; // [G][w+1]
+        double* const xR = ringR + (std::size_t)G * ws;
+        if (KIND == kUp && sx) __syncthreads(); // state staging reads done
+        double* eL = sx ? xL + g * ws : oL;
+        double* eR = sx ? xR + g * ws : oR;
+        fexport(c, vl, vr, 0, eL, eR, live);
+        fcontract<Q, U>(c, vl, vr, m + 1, 2 * m, fo, eL, eR, live);
+        if (sx) {
+            __syncthreads();
+            double* gL = a.out_L + (std::size_t)bfirst * w;
+            double* gR = a.out_R + (std::size_t)bfirst * w;
+            for (int j = t; j < ntiles * w; j += nt) {
+                const int gg = j / w, i = j - gg * w;
+                gL[j] = xL[gg * ws + i];
+                gR[j] = xR[gg * ws + i];
+            }
+        }
     } else {
         __syncthreads(); // ring reads done before the staging reuses it
         double* my = stage + g * ws;
@@ -625,16 +670,17 @@ int tiles_per_cta(int w, int p) {
     return G;
 }
 
-template <int P, int MAXT = 256, int MINB = 1, int U = 1>
+template <int P, int MAXT = 256, int MINB = 1, int U = 1, bool XS = false>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     static_assert(P % 2 == 0, "the folded layout holds P/2 distance pairs per thread");
+    if (XS != (a.m <= kXportLevels)) return cudaErrorInvalidValue;
     const int tt = a.w / P;
     const int G = tiles_per_cta(a.w, P);
     const int nt = G * tt;
     const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
-    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U>
-                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U>
-                                                        : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U>;
+    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS>
+                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS>
+                                                        : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -709,12 +755,15 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
         }
     }
     if (a.w / a.p > 256) return a.p == 2 ? launch_tile_p<2, 1024>(kind, a, st) : cudaErrorInvalidValue;
+    const bool xs = a.m <= kXportLevels; // short tiles: staged exports (XS build)
     switch (a.p) {
-    case 2: return launch_tile_p<2>(kind, a, st);
-    case 4: return launch_tile_p<4>(kind, a, st); // (w = 32: caps/unroll measured slower)
+    case 2: return xs ? launch_tile_p<2, 256, 1, 1, true>(kind, a, st) : launch_tile_p<2>(kind, a, st);
+    case 4: // (w = 32: register caps / unroll measured slower)
+        return xs ? launch_tile_p<4, 256, 1, 1, true>(kind, a, st) : launch_tile_p<4>(kind, a, st);
     case 8: // measured (w = 64 .. 2048): 64-register cap (4 CTAs/SM) + unroll 2
-        return a.w >= 64 ? launch_tile_p<8, 256, 4, 2>(kind, a, st) : launch_tile_p<8>(kind, a, st);
-    case 16: return launch_tile_p<16>(kind, a, st);
+        if (a.w < 64) return launch_tile_p<8, 256, 1, 1, true>(kind, a, st);
+        return xs ? launch_tile_p<8, 256, 4, 2, true>(kind, a, st) : launch_tile_p<8, 256, 4, 2>(kind, a, st);
+    case 16: return xs ? launch_tile_p<16, 256, 1, 1, true>(kind, a, st) : launch_tile_p<16>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
 }
