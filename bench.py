@@ -200,7 +200,7 @@ def run_b200(args, rank, world):
 
     if s1d.device_count() == 0:
         raise SystemExit("bench.py: no CUDA device visible (the B200 path has no CPU fallback)")
-    local = env_int("LOCAL_RANK", 0)
+    local = env_int("LOCAL_RANK", 0) % s1d.device_count()  # this rank's GPU
     n_per = 1 << args.log2n
     eq = s1d.Equation.Heat if args.equation == "heat" else s1d.Equation.Euler
     scheme = s1d.Scheme.Swept if args.scheme == "swept" else s1d.Scheme.Classic

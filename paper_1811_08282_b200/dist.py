@@ -34,7 +34,9 @@ def open_ring_shard(cfg, rank: Optional[int] = None, world: Optional[int] = None
     from .api import InvalidConfig, Shard
     rank = dist.get_rank(group) if rank is None else rank
     world = dist.get_world_size(group) if world is None else world
-    device = int(os.environ.get("LOCAL_RANK", rank)) if device is None else device
+    if device is None:  # one GPU per local rank (wraps when ranks outnumber GPUs, e.g. tests)
+        from .api import device_count
+        device = int(os.environ.get("LOCAL_RANK", rank)) % max(1, device_count())
     if cfg.ranks != world:
         raise InvalidConfig(f"cfg.ranks={cfg.ranks} must equal the process count {world}")
     shard = Shard(cfg, rank, device)

@@ -1,4 +1,4 @@
-"""GPU multi-device parity (skipped with fewer than 2 GPUs):
+"""GPU multi-device parity (single-device cases run anywhere; the rest need 2 GPUs):
   * single process, shards on several devices (ranks = G, num_devices = G);
   * one process per GPU (torchrun + CUDA IPC + device flags): tools/mp_check.py.
 """
@@ -41,12 +41,23 @@ def test_single_process_multi_device(gpu, eq, method, scheme, ranks, wf):
     assert np.array_equal(bits(got), bits(O.port_run_serial(eq, method, n=n, steps=T)))
 
 
-@need2
-def test_multi_process_torchrun(gpu):
-    nproc = 2
+def _torchrun_mp_check(nproc, port):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
-           "--master-addr", "127.0.0.1", "--master-port", "29517", os.path.join(ROOT, "tools", "mp_check.py")]
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "tools", "mp_check.py")]
     r = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=600)
     print(r.stdout[-4000:], r.stderr[-4000:])
     assert r.returncode == 0
-    assert r.stdout.count("ok ") >= 9
+    assert "BAD" not in r.stdout
+    return r.stdout.count("ok ")
+
+
+@need2
+def test_multi_process_torchrun(gpu):
+    # one process per GPU, the bench contract's launch mode
+    assert _torchrun_mp_check(2, 29517) >= 13
+
+
+def test_multi_process_ranks_share_gpus(gpu):
+    # more ranks than GPUs (ranks wrap onto devices): the CUDA IPC + device
+    # flag ring with 4 processes, runnable on a single-GPU box
+    assert _torchrun_mp_check(4, 29518) >= 12

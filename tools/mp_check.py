@@ -24,6 +24,11 @@ CASES = [
     ("euler", "lengthening", "classic", 1 << 12, 64, 0, 40),
     ("euler", "flattening", "swept", 1 << 12, 128, 0, 111),
     ("euler", "flattening", "classic", 1 << 12, 64, 0, 30),
+    # 96 blocks: partitions for 2, 3, 4, 6 and 8 ranks
+    ("heat", "lengthening", "swept", 96 * 64, 64, 0, 333),
+    ("heat", "lengthening", "classic", 96 * 64, 64, 0, 50),
+    ("euler", "lengthening", "swept", 96 * 64, 64, 0, 77),
+    ("euler", "flattening", "swept", 96 * 64, 64, 0, 61),
 ]
 
 
@@ -38,6 +43,12 @@ def main():
                                method=s1d.Method.Lengthening if me == "lengthening" else s1d.Method.Flattening,
                                scheme=s1d.Scheme.Swept if sc == "swept" else s1d.Scheme.Classic, grid_size=n,
                                block_width=w, ranks=world, work_factor=wf, steps=T)
+        try:
+            s1d.make_partition(cfg)
+        except s1d.InvalidConfig:  # e.g. WF shares that do not divide the blocks at this world size
+            if rank == 0:
+                print(f"skip {eq} {me} {sc} n={n} w={w} wf={wf}: no partition for {world} ranks", flush=True)
+            continue
         with open_ring_shard(cfg) as shard:
             out, st, tm = shard.solve()
             out2, _, _ = shard.solve()  # repeated runs stay in lockstep
