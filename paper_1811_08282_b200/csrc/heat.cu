@@ -66,101 +66,18 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
     }
 }
 
-// Incoming edges stream through a per-tile ring of kRing levels (2 values per
-// level per side) filled with cp.async kRing-2 levels ahead of use, so shared
-// memory per tile is O(1) in w. The ring index of (level r, x) is affine in x
-// and wrapped with a mask.
+// Incoming edges stream through a per-tile ring of at most kRing levels (2
+// values per level per side) filled with cp.async kRing-2 levels ahead of
+// use, so shared memory per tile is O(1) in w (S1D_HEAT_RING: build knob).
 #ifndef S1D_HEAT_RING
 #define S1D_HEAT_RING 16
 #endif
-constexpr int kRing = S1D_HEAT_RING;  // levels held per side (power of two)
+constexpr int kRing = S1D_HEAT_RING; // levels held per side (power of two)
 constexpr int kRingMask = 2 * kRing - 1;
-__host__ __device__ inline int tile_edge_stride(int) { return 4 * kRing; }
 
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
-
-template <int P>
-struct TileCtx {
-    int w, m, tt, lt;     // width, levels, threads per tile, thread-in-tile
-    int my_lo;            // x of v[0]
-    int wlo, whi;         // x range of my warp (superset if it spans tiles)
-    double* XL;           // exchange: last values, [2][G*(tt+2)]
-    double* XF;           // exchange: first values
-    int xs;               // parity stride of XL/XF
-    int slot;             // my slot (tile base + lt + 1)
-    const double* einR;   // my tile's ring of left-producer R edges [kRing][2]
-    const double* einL;   // ring of right-producer L edges
-};
-
-template <int P>
-__device__ __forceinline__ void publish(const TileCtx<P>& c, const double (&v)[P], int r) {
-    const int par = (r & 1) * c.xs;
-    c.XF[par + c.slot] = v[0];
-    c.XL[par + c.slot] = v[P - 1];
-}
-
-template <int P>
-__device__ __forceinline__ void compute_level(const TileCtx<P>& c, double (&v)[P], int r, int lo, int hi,
-                                              double fo) {
-    if (c.whi >= lo && c.wlo < hi) {
-        const int par = (r & 1) * c.xs;
-        const double lft = c.XL[par + c.slot - 1];
-        const double rgt = c.XF[par + c.slot + 1];
-        double nv[P];
-        if (P == 1) {
-            nv[0] = heat_f(lft, v[0], rgt, fo);
-        } else {
-            nv[0] = heat_f(lft, v[0], v[1], fo);
-#pragma unroll
-            for (int k = 1; k < P - 1; ++k) nv[k] = heat_f(v[k - 1], v[k], v[k + 1], fo);
-            nv[P - 1] = heat_f(v[P - 2], v[P - 1], rgt, fo);
-        }
-#pragma unroll
-        for (int k = 0; k < P; ++k) v[k] = nv[k];
-    }
-}
-
-// Exports of level r (contracting half, d = r - m): L[d] = x in {lo, lo+1},
-// R[d] = x in {hi-2, hi-1}; edge layout [level][2].
-template <int P>
-__device__ __forceinline__ void export_level(const TileCtx<P>& c, const double (&v)[P], int d, int lo, int hi,
-                                             double* oL, double* oR) {
-    if (c.wlo <= lo + 1 && c.whi >= lo) {
-        double* dst = oL + 2 * d - lo + c.my_lo; // address of x = my_lo + k is dst + k
-#pragma unroll
-        for (int k = 0; k < P; ++k)
-            if ((unsigned)(c.my_lo + k - lo) < 2u) dst[k] = v[k];
-    }
-    if (c.wlo <= hi - 1 && c.whi >= hi - 2) {
-        double* dst = oR + 2 * d - (hi - 2) + c.my_lo;
-#pragma unroll
-        for (int k = 0; k < P; ++k)
-            if ((unsigned)(c.my_lo + k - (hi - 2)) < 2u) dst[k] = v[k];
-    }
-}
-
-// Inserts of level r (expanding half): left producer's R[r-1] at x = lo-1, lo
-// and right producer's L[r-1] at x = hi-1, hi. Points beyond (x < lo-1,
-// x > hi) are outside the dependency cone and may take any value, so one-sided
-// predicates suffice and the smem address stays affine in x.
-template <int P>
-__device__ __forceinline__ void insert_level(const TileCtx<P>& c, double (&v)[P], int r, int lo, int hi) {
-    if (c.wlo <= lo && c.whi >= lo - 1) {
-        // ring index of x at level r: 2(r-1) + x - (lo-1)
-        const int base = 2 * (r - 1) - (lo - 1) + c.my_lo;
-#pragma unroll
-        for (int k = 0; k < P; ++k)
-            if (c.my_lo + k <= lo) v[k] = c.einR[(base + k) & kRingMask];
-    }
-    if (c.whi >= hi - 1 && c.wlo <= hi) {
-        const int base = 2 * (r - 1) - (hi - 1) + c.my_lo;
-#pragma unroll
-        for (int k = 0; k < P; ++k)
-            if (c.my_lo + k >= hi - 1) v[k] = c.einL[(base + k) & kRingMask];
-    }
-}
 
 // Diagnostic builds (-DS1D_NO_LEVEL_BARRIER) replace the level barrier with
 // __syncwarp() to time the level loop without it (results are then wrong).
@@ -541,6 +458,93 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
             if (gp < a.N) a.state_out[gp] = val;
             else a.state_right[gp - a.N] = val;
         }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Debug-kernel helpers: the contiguous layout (tile thread lt owns x = 1 +
+// lt*P + k), an independent restatement of the tile geometry.
+// ---------------------------------------------------------------------------
+__host__ __device__ inline int tile_edge_stride(int) { return 4 * kRing; }
+
+template <int P>
+struct TileCtx {
+    int w, m, tt, lt;     // width, levels, threads per tile, thread-in-tile
+    int my_lo;            // x of v[0]
+    int wlo, whi;         // x range of my warp (superset if it spans tiles)
+    double* XL;           // exchange: last values, [2][G*(tt+2)]
+    double* XF;           // exchange: first values
+    int xs;               // parity stride of XL/XF
+    int slot;             // my slot (tile base + lt + 1)
+    const double* einR;   // my tile's ring of left-producer R edges [kRing][2]
+    const double* einL;   // ring of right-producer L edges
+};
+
+template <int P>
+__device__ __forceinline__ void publish(const TileCtx<P>& c, const double (&v)[P], int r) {
+    const int par = (r & 1) * c.xs;
+    c.XF[par + c.slot] = v[0];
+    c.XL[par + c.slot] = v[P - 1];
+}
+
+template <int P>
+__device__ __forceinline__ void compute_level(const TileCtx<P>& c, double (&v)[P], int r, int lo, int hi,
+                                              double fo) {
+    if (c.whi >= lo && c.wlo < hi) {
+        const int par = (r & 1) * c.xs;
+        const double lft = c.XL[par + c.slot - 1];
+        const double rgt = c.XF[par + c.slot + 1];
+        double nv[P];
+        if (P == 1) {
+            nv[0] = heat_f(lft, v[0], rgt, fo);
+        } else {
+            nv[0] = heat_f(lft, v[0], v[1], fo);
+#pragma unroll
+            for (int k = 1; k < P - 1; ++k) nv[k] = heat_f(v[k - 1], v[k], v[k + 1], fo);
+            nv[P - 1] = heat_f(v[P - 2], v[P - 1], rgt, fo);
+        }
+#pragma unroll
+        for (int k = 0; k < P; ++k) v[k] = nv[k];
+    }
+}
+
+// Exports of level r (contracting half, d = r - m): L[d] = x in {lo, lo+1},
+// R[d] = x in {hi-2, hi-1}; edge layout [level][2].
+template <int P>
+__device__ __forceinline__ void export_level(const TileCtx<P>& c, const double (&v)[P], int d, int lo, int hi,
+                                             double* oL, double* oR) {
+    if (c.wlo <= lo + 1 && c.whi >= lo) {
+        double* dst = oL + 2 * d - lo + c.my_lo; // address of x = my_lo + k is dst + k
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if ((unsigned)(c.my_lo + k - lo) < 2u) dst[k] = v[k];
+    }
+    if (c.wlo <= hi - 1 && c.whi >= hi - 2) {
+        double* dst = oR + 2 * d - (hi - 2) + c.my_lo;
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if ((unsigned)(c.my_lo + k - (hi - 2)) < 2u) dst[k] = v[k];
+    }
+}
+
+// Inserts of level r (expanding half): left producer's R[r-1] at x = lo-1, lo
+// and right producer's L[r-1] at x = hi-1, hi. Points beyond (x < lo-1,
+// x > hi) are outside the dependency cone and may take any value, so one-sided
+// predicates suffice and the smem address stays affine in x.
+template <int P>
+__device__ __forceinline__ void insert_level(const TileCtx<P>& c, double (&v)[P], int r, int lo, int hi) {
+    if (c.wlo <= lo && c.whi >= lo - 1) {
+        // ring index of x at level r: 2(r-1) + x - (lo-1)
+        const int base = 2 * (r - 1) - (lo - 1) + c.my_lo;
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (c.my_lo + k <= lo) v[k] = c.einR[(base + k) & kRingMask];
+    }
+    if (c.whi >= hi - 1 && c.wlo <= hi) {
+        const int base = 2 * (r - 1) - (hi - 1) + c.my_lo;
+#pragma unroll
+        for (int k = 0; k < P; ++k)
+            if (c.my_lo + k >= hi - 1) v[k] = c.einL[(base + k) & kRingMask];
     }
 }
 
