@@ -1,0 +1,91 @@
+"""GPU parity at the BASELINE sizes (configs 1-2), through size-independent
+properties — the CPU oracle cannot run 2^27 points x thousands of steps:
+
+  * heat n = 2^27: swept (w = 1024 and the short-tile path, w = 32) ==
+    classic, bit for bit; and windows of the result == an exact FTCS
+    restatement run on the window's dependency cone (the value at x after T
+    steps depends only on [x-T, x+T]; numpy float64 evaluates
+    c + fo*((l - 2c) + r) with one IEEE rounding per operation, like the
+    reference's -ffp-contract=off build);
+  * Euler Sod n = 2^22: lengthening swept == flattening swept == classic,
+    bit for bit, and mass conserved.
+"""
+import numpy as np
+import pytest
+
+import paper_1811_08282_b200 as s1d
+
+pytestmark = pytest.mark.gpu
+
+N_HEAT = 1 << 27
+HEAT_SPEC = s1d.make_spec(s1d.Equation.Heat, s1d.Method.Lengthening)
+T_HEAT = 1024
+
+
+def bits(a):
+    return np.ascontiguousarray(a).view(np.uint64)
+
+
+def heat(scheme, w, steps=T_HEAT, n=N_HEAT):
+    return s1d.run(s1d.LaunchConfig(equation=s1d.Equation.Heat, scheme=scheme, grid_size=n, block_width=w, ranks=1,
+                                    steps=steps, mode=s1d.Mode.WallClock)).state
+
+
+def ftcs_window(x0, x1, n, steps, fo=0.4):
+    """Exact heat_step (inc/kernels.hpp:14-16) on the cone of [x0, x1)."""
+    lo = x0 - steps
+    idx = np.arange(lo, x1 + steps) % n
+    u = np.empty(idx.size)
+    # the IC restated by the library's host code (bitwise == partition.cpp, tests/test_host.py)
+    for a, b in _runs(idx):
+        u[a:b] = s1d.initial_condition_range("heat-sine", n, HEAT_SPEC, int(idx[a]), b - a)
+    for _ in range(steps):
+        l, c, r = u[:-2], u[1:-1], u[2:]
+        u = c + fo * ((l - 2.0 * c) + r)
+    return u  # covers [x0, x1)
+
+
+def _runs(idx):
+    """Split a wrapped index array into contiguous ascending runs."""
+    cuts = np.nonzero(np.diff(idx) != 1)[0] + 1
+    starts = np.concatenate(([0], cuts))
+    ends = np.concatenate((cuts, [idx.size]))
+    return zip(starts.tolist(), ends.tolist())
+
+
+@pytest.fixture(scope="module")
+def heat_swept_1024():
+    return heat(s1d.Scheme.Swept, 1024)
+
+
+def test_heat_2p27_swept_equals_classic(heat_swept_1024):
+    classic = heat(s1d.Scheme.Classic, 1024)
+    assert np.array_equal(bits(heat_swept_1024), bits(classic))
+
+
+def test_heat_2p27_short_tiles_equal_wide(heat_swept_1024):
+    assert np.array_equal(bits(heat(s1d.Scheme.Swept, 32)), bits(heat_swept_1024))
+
+
+@pytest.mark.parametrize("x0", [0, N_HEAT // 2 - 700, N_HEAT - 512])
+def test_heat_2p27_windows_match_exact_ftcs(heat_swept_1024, x0):
+    want = ftcs_window(x0, x0 + 1024, N_HEAT, T_HEAT)
+    got = heat_swept_1024[np.arange(x0, x0 + 1024) % N_HEAT]
+    assert np.array_equal(bits(got), bits(want))
+
+
+def euler(method, scheme, n=1 << 22, w=512, steps=512):
+    cfg = s1d.LaunchConfig(equation=s1d.Equation.Euler, method=method, scheme=scheme, grid_size=n, block_width=w,
+                           ranks=1, steps=steps, mode=s1d.Mode.WallClock)
+    return s1d.run(cfg).state
+
+
+def test_euler_2p22_swept_classic_flat_len_agree(gpu):
+    L, F = s1d.Method.Lengthening, s1d.Method.Flattening
+    ref = euler(L, s1d.Scheme.Swept)
+    assert np.array_equal(bits(euler(F, s1d.Scheme.Swept)), bits(ref))
+    assert np.array_equal(bits(euler(L, s1d.Scheme.Classic)), bits(ref))
+    rho = ref.reshape(-1, 3)[:, 0]
+    spec = s1d.make_spec(s1d.Equation.Euler, s1d.Method.Lengthening)
+    ic = s1d.initial_condition("euler-sod-periodic", 1 << 22, spec).reshape(-1, 3)
+    assert abs(rho.sum() - ic[:, 0].sum()) <= 1e-12 * ic[:, 0].sum()
