@@ -67,6 +67,8 @@ def port():
         lib.s1o_max_signal_speed.argtypes = [_dp, C.c_size_t, C.c_double, _dp]
         lib.s1o_run_serial.argtypes = [C.c_int, C.c_int, C.c_size_t, C.c_long, C.c_double, C.c_double,
                                        C.c_double, C.c_double, C.c_char_p, _dp]
+        lib.s1o_run_state.argtypes = [C.c_int, C.c_int, C.c_size_t, C.c_long, C.c_double, C.c_double, C.c_double,
+                                      _dp, _dp]
         lib.s1o_fnv1a64.restype = C.c_ulonglong
         lib.s1o_fnv1a64.argtypes = [_dp, C.c_size_t]
         _port = lib
@@ -84,6 +86,18 @@ def port_run_serial(equation="heat", method="lengthening", n=1024, steps=50, fou
                                fourier, gamma, dt_dx, cfl, initial.encode(), _ptr(out))
     if st:
         raise OracleError(st, "port run_serial failed")
+    return out
+
+
+def port_run_state(equation, method, ic: np.ndarray, steps: int, dt_dx: float, fourier=0.4, gamma=1.4) -> np.ndarray:
+    """serial_advance from a given periodic state (s1o_run_state)."""
+    ic = np.ascontiguousarray(ic, dtype=np.float64)
+    n = ic.size // vpp(equation)
+    out = np.empty_like(ic)
+    st = port().s1o_run_state(0 if equation == "heat" else 1, 0 if method == "lengthening" else 1, n, steps, fourier,
+                              gamma, dt_dx, _ptr(ic), _ptr(out))
+    if st:
+        raise OracleError(st, "port run_state failed")
     return out
 
 

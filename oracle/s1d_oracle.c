@@ -232,7 +232,6 @@ int s1o_run_serial(int equation, int method, size_t n, long steps, double fourie
     const int heat = equation == 0;
     const int flat = !heat && method == 1;
     const size_t h = flat ? 2 : 1;
-    const long S = heat ? 1 : (flat ? 2 : 4);
     const int vpp = heat ? 1 : 3;
     /* LaunchConfig::validate(partitioned=false), src/config.cpp:45-62 */
     if (n < 2 * h + 1 || steps < 0 || !(fourier > 0.0) || fourier > 0.5 || !(gamma > 1.0)) return S1O_INVALID_CONFIG;
@@ -253,6 +252,19 @@ int s1o_run_serial(int equation, int method, size_t n, long steps, double fourie
         }
         dt_dx = cfl / smax;
     }
+    st = s1o_run_state(equation, method, n, steps, fourier, gamma, dt_dx, ic, out);
+    free(ic);
+    return st;
+}
+
+/* serial_advance (engines_impl.hpp:85-128) from a given state. */
+int s1o_run_state(int equation, int method, size_t n, long steps, double fourier, double gamma, double dt_dx,
+                  const double* ic, double* out) {
+    const int heat = equation == 0;
+    const int flat = !heat && method == 1;
+    const size_t h = flat ? 2 : 1;
+    const long S = heat ? 1 : (flat ? 2 : 4);
+    if (n < 2 * h + 1 || steps < 0) return S1O_INVALID_CONFIG;
 
     soa_t a;
     a.nf = heat ? 2 : (flat ? 6 : 7);
@@ -265,10 +277,9 @@ int s1o_run_serial(int equation, int method, size_t n, long steps, double fourie
             for (int k = 0; k < 3; ++k) a.f[k][h + j] = a.f[3 + k][h + j] = ic[3 * j + (size_t)k];
         }
     }
-    free(ic);
 
     const long total = steps * S;
-    st = S1O_OK;
+    int st = S1O_OK;
     for (long c = 1; c <= total && !st; ++c) {
         refresh_halo(&a, n, h);
         if (heat) {

@@ -47,6 +47,12 @@ int s1o_max_signal_speed(const double* prim, size_t len, double gamma, double* o
 int s1o_run_serial(int equation, int method, size_t n, long steps, double fourier, double gamma,
                    double dt_dx, double cfl, const char* initial, double* out);
 
+/* The same periodic solver from a caller-given state (n*vpp doubles) with an
+ * explicit dt_dx (no finalize): the windowed full-size parity tests run it on
+ * a point's dependency cone. */
+int s1o_run_state(int equation, int method, size_t n, long steps, double fourier, double gamma, double dt_dx,
+                  const double* ic, double* out);
+
 /* FNV-1a 64 over the little-endian bytes of `count` doubles. */
 unsigned long long s1o_fnv1a64(const double* v, size_t count);
 

@@ -8,12 +8,15 @@ properties — the CPU oracle cannot run 2^27 points x thousands of steps:
     c + fo*((l - 2c) + r) with one IEEE rounding per operation, like the
     reference's -ffp-contract=off build);
   * Euler Sod n = 2^22: lengthening swept == flattening swept == classic,
-    bit for bit, and mass conserved.
+    bit for bit, mass conserved, and windows (across both Sod jumps) == the C
+    oracle run on the window's cone (4 cells per step for both methods) with
+    the full problem's dt/dx.
 """
 import numpy as np
 import pytest
 
 import paper_1811_08282_b200 as s1d
+from oracle import oracle as O
 
 pytestmark = pytest.mark.gpu
 
@@ -80,9 +83,32 @@ def euler(method, scheme, n=1 << 22, w=512, steps=512):
     return s1d.run(cfg).state
 
 
-def test_euler_2p22_swept_classic_flat_len_agree(gpu):
+N_EU, T_EU = 1 << 22, 512
+
+
+@pytest.fixture(scope="module")
+def euler_len_swept():
+    return euler(s1d.Method.Lengthening, s1d.Scheme.Swept, n=N_EU, steps=T_EU)
+
+
+@pytest.mark.parametrize("method", ["lengthening", "flattening"])
+@pytest.mark.parametrize("x0", [-32, N_EU // 2 - 32, N_EU // 2 + 1500])
+def test_euler_2p22_windows_match_oracle(euler_len_swept, method, x0):
+    cfg = s1d.LaunchConfig(equation=s1d.Equation.Euler, grid_size=N_EU, block_width=512, ranks=1, steps=T_EU)
+    cfg.finalize()  # dt/dx of the full problem (cfl / max signal speed of the whole IC)
+    spec = s1d.make_spec(s1d.Equation.Euler, s1d.Method.Lengthening)
+    pad, W = 4 * T_EU + 8, 64
+    idx = np.arange(x0 - pad, x0 + W + pad) % N_EU
+    ic = np.concatenate([s1d.initial_condition_range("euler-sod-periodic", N_EU, spec, a, b - a)
+                         for a, b in ((int(idx[i]), int(idx[j - 1]) + 1) for i, j in _runs(idx))])
+    want = O.port_run_state("euler", method, ic, T_EU, cfg.phys.dt_dx).reshape(-1, 3)[pad:pad + W]
+    got = euler_len_swept.reshape(-1, 3)[np.arange(x0, x0 + W) % N_EU]
+    assert np.array_equal(bits(got), bits(want))
+
+
+def test_euler_2p22_swept_classic_flat_len_agree(euler_len_swept):
     L, F = s1d.Method.Lengthening, s1d.Method.Flattening
-    ref = euler(L, s1d.Scheme.Swept)
+    ref = euler_len_swept
     assert np.array_equal(bits(euler(F, s1d.Scheme.Swept)), bits(ref))
     assert np.array_equal(bits(euler(L, s1d.Scheme.Classic)), bits(ref))
     rho = ref.reshape(-1, 3)[:, 0]
