@@ -704,11 +704,14 @@ int heat_points_per_thread(int w) {
         if ((p == 2 || p == 4 || p == 8 || p == 16) && w % p == 0 && w / p <= 256) return p;
     }
     // Folded layout: P even (P/2 distance pairs per thread). Measured on B200
-    // (n = 2^27): P = 8 is fastest from w = 64 up, P = 4 at w = 32; wide tiles
-    // double P until w/P <= 256 threads. Always P | w, w/P <= 256 except for
-    // w = 2 mod 4 (P = 2, up to 1024 threads).
+    // (n = 2^27, each with its register cap / unroll): P = 16 from w = 128
+    // (twice the work per level barrier of P = 8: +9% at w = 1024), P = 8 at
+    // w = 32..64 or when 16 does not divide w, else P = 4; wide tiles double P
+    // until w/P <= 256 threads. Always P | w, w/P <= 256 except for w = 2 mod 4
+    // (P = 2, up to 1024 threads).
     int p = 2;
-    if (w % 8 == 0 && w >= 64) p = 8;
+    if (w % 16 == 0 && w >= 128) p = 16;
+    else if (w % 8 == 0 && w >= 32) p = 8;
     else if (w % 4 == 0) p = 4;
     while (w / p > 256 && w % (2 * p) == 0 && p < 16) p *= 2;
     if (w / p > 1024) return -1; // no valid decomposition (caller reports it)
@@ -764,10 +767,12 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     case 2: return xs ? launch_tile_p<2, 256, 1, 1, true>(kind, a, st) : launch_tile_p<2>(kind, a, st);
     case 4: // (w = 32: register caps / unroll measured slower)
         return xs ? launch_tile_p<4, 256, 1, 1, true>(kind, a, st) : launch_tile_p<4>(kind, a, st);
-    case 8: // measured (w = 64 .. 2048): 64-register cap (4 CTAs/SM) + unroll 2
-        if (a.w < 64) return launch_tile_p<8, 256, 1, 1, true>(kind, a, st);
+    case 8: // measured (w = 64 and widths 16 does not divide): 64-register cap (4 CTAs/SM) + unroll 2
+        if (a.w < 64) return launch_tile_p<8, 256, 1, 2, true>(kind, a, st); // w = 32: unroll only
         return xs ? launch_tile_p<8, 256, 4, 2, true>(kind, a, st) : launch_tile_p<8, 256, 4, 2>(kind, a, st);
-    case 16: return xs ? launch_tile_p<16, 256, 1, 1, true>(kind, a, st) : launch_tile_p<16>(kind, a, st);
+    case 16: // measured (n = 2^27): 4 CTAs/SM + unroll 2 from w = 256 (1.95-1.97 T), 3 CTAs/SM at w = 128
+        if (xs) return launch_tile_p<16, 256, 1, 1, true>(kind, a, st);
+        return a.w >= 256 ? launch_tile_p<16, 256, 4, 2>(kind, a, st) : launch_tile_p<16, 256, 3, 1>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
 }
