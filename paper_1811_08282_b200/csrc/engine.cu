@@ -159,7 +159,10 @@ struct Solver {
         m = cycle_advance(cfg.block_width, static_cast<std::uint64_t>(spec.h));
         if (cfg.scheme == S1D_SWEPT) {
             if (!euler) {
-                p = heat_points_per_thread(static_cast<int>(cfg.block_width));
+                long long min_tiles = -1;
+                for (std::uint64_t bk : part.blocks)
+                    if (min_tiles < 0 || static_cast<long long>(bk) < min_tiles) min_tiles = static_cast<long long>(bk);
+                p = heat_points_per_thread(static_cast<int>(cfg.block_width), min_tiles);
                 if (p < 0)
                     throw Error(S1D_INVALID_WIDTH,
                                 "block width " + std::to_string(cfg.block_width) +

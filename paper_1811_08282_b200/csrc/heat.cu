@@ -698,7 +698,7 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
 
 } // namespace
 
-int heat_points_per_thread(int w) {
+int heat_points_per_thread(int w, long long tiles) {
     if (const char* e = std::getenv("S1D_HEAT_P")) {
         const int p = std::atoi(e);
         if ((p == 2 || p == 4 || p == 8 || p == 16) && w % p == 0 && w / p <= 256) return p;
@@ -715,6 +715,22 @@ int heat_points_per_thread(int w) {
     else if (w % 4 == 0) p = 4;
     while (w / p > 256 && w % (2 * p) == 0 && p < 16) p *= 2;
     if (w / p > 1024) return -1; // no valid decomposition (caller reports it)
+    // Small grids: P = 16 packs twice the tiles per CTA of P = 8; below one
+    // full wave (4 CTAs per SM) P = 8 fills the GPU better (measured n = 2^20:
+    // 1.29-1.32 T with P = 8 vs 1.01-1.04 T with P = 16 at w = 256..1024).
+    if (p == 16 && tiles >= 0 && w / 8 <= 256) {
+        static int sms = 0;
+        if (sms == 0) {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) {
+                cudaGetLastError();
+                sms = 148;
+            }
+        }
+        const long long g = tiles_per_cta(w, 16);
+        if ((tiles + g - 1) / g < 4LL * sms) p = 8;
+    }
     return p;
 }
 

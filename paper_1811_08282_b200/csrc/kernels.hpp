@@ -72,7 +72,9 @@ struct ClassicArgs {
 // `debug` selects the instrumented instantiation (coverage / perturb).
 cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st);
 cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool debug = false);
-int heat_points_per_thread(int w);
+// Points per thread of the heat tile kernel for width w; `tiles` (the
+// smallest shard's tile count, or -1) lets small grids trade P for CTAs.
+int heat_points_per_thread(int w, long long tiles = -1);
 
 // Euler (flat = 0 lengthening, 1 flattening). Classic kernels update `out`
 // in place (fields written by a substep are never read by it).
