@@ -4,7 +4,7 @@
 //   make_partition / extents / IC     src/partition.cpp:10-113
 //   cycle_advance / schedules         src/swept.cpp:11-64
 // Errors are thrown as s1d::Error{status, message} and converted to status
-// codes at the C ABI (capi.cpp).
+// codes at the C ABI (engine.cu, extern "C" section).
 #pragma once
 
 #include <cstdint>
