@@ -12,4 +12,35 @@ __device__ __forceinline__ double next_up(double x) {
     return __longlong_as_double(x > 0.0 ? b + 1 : b - 1);
 }
 
+// Round hand-off between shards of different processes (one process per GPU):
+// a shard's flag word holds the rounds completed by one ring neighbour, stored
+// by that neighbour over NVLink (system-scope release) and polled here
+// (system-scope acquire). The spin is bounded: after timeout_ns it sets bit 1
+// of *err and returns, so a dead peer cannot wedge the GPU.
+__device__ __forceinline__ unsigned flag_ld_acquire(const unsigned* p) {
+    unsigned v;
+    asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void flag_st_release(unsigned* p, unsigned v) {
+    asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void flag_wait(const unsigned* f, unsigned seq, int* err, unsigned long long timeout_ns) {
+    if ((int)(flag_ld_acquire(f) - seq) >= 0) return;
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while ((int)(flag_ld_acquire(f) - seq) < 0) {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        if (t - t0 > timeout_ns) {
+            atomicOr(err, 2);
+            return;
+        }
+    }
+}
+__device__ __forceinline__ void flag_signal(unsigned* f, unsigned seq) {
+    __threadfence_system();
+    flag_st_release(f, seq);
+}
+
 } // namespace s1d

@@ -500,8 +500,17 @@ struct Solver {
         // cur[g]: buffer holding shard g's current level; heat ping-pongs
         // through state[0]/state[1] (cur_idx: which one holds the result, -1 =
         // ic); Euler updates state[0] in place.
+        // One process per GPU: the round's hand-off is fused into the substep
+        // kernel (its boundary points wait / signal, kernels.hpp ClassicArgs),
+        // one launch per round instead of wait + substep + signal.
+        const bool fused = mp && R() > 1;
+        // The previous round may have written into this shard's state from a
+        // neighbour (a seam-centred DownTriangle spills its right half into the
+        // right shard's array; the pad runs right after it), and interior
+        // points do not wait in a fused round: one full wait first.
+        if (fused && c_begin <= c_end) wait_neighbours();
         for (std::int64_t c = c_begin; c <= c_end; ++c) {
-            wait_neighbours();
+            if (!fused) wait_neighbours();
             if (dominant && c == c_begin) record_all(&Shard::ev_dom0);
             const int nxt = euler ? 0 : ((*cur_idx == 0) ? 1 : 0);
             for (int g : locals) {
@@ -526,13 +535,22 @@ struct Solver {
                 a.dt_dx = cfg.dt_dx;
                 a.error_flag = s.err;
                 a.dbg = dbg_args(g);
+                if (fused) {
+                    a.nb_flags = s.flags;
+                    a.wait_seq = seq;
+                    a.sig_seq = seq + 1;
+                    a.sig_left = L.flags + 1; // I am my left neighbour's right neighbour
+                    a.sig_right = Rt.flags + 0;
+                    a.timeout_ns = kRoundTimeoutNs;
+                }
                 S1D_CUDA(cudaSetDevice(s.dev));
                 if (euler) S1D_CUDA(launch_euler_classic(flat ? 1 : 0, a, s.st));
                 else S1D_CUDA(launch_heat_classic(a, s.st));
                 stats.kernel_launches += 1;
             }
             if (dominant && c == c_end) record_all(&Shard::ev_dom1);
-            record_round();
+            if (fused) ++seq;
+            else record_round();
             *cur_idx = nxt;
             for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).state[nxt];
         }

@@ -65,6 +65,24 @@ __device__ __forceinline__ void classic_count(const ClassicArgs& a, std::uint64_
     atomicAdd(a.dbg.cov + (std::uint64_t)(a.counter - 1) * a.dbg.cov_n + (a.dbg.gstart + x) % a.dbg.cov_n, 1u);
 }
 
+// One process per GPU: the first / last block of the shard waits for the
+// neighbour's previous round before its first halo read, and signals this
+// round after the block's final barrier (its boundary records are stored;
+// other blocks neither read nor write what the neighbours touch).
+__device__ __forceinline__ void classic_round_wait(const ClassicArgs& a, bool lb, bool rb) {
+    if (!a.nb_flags || !(lb || rb)) return;
+    if (threadIdx.x == 0) {
+        if (lb) flag_wait(a.nb_flags, a.wait_seq, a.error_flag, a.timeout_ns);
+        if (rb) flag_wait(a.nb_flags + 1, a.wait_seq, a.error_flag, a.timeout_ns);
+    }
+    __syncthreads();
+}
+__device__ __forceinline__ void classic_round_signal(const ClassicArgs& a, bool lb, bool rb) {
+    if (!a.nb_flags || threadIdx.x != 0) return;
+    if (lb) flag_signal(a.sig_left, a.sig_seq);
+    if (rb) flag_signal(a.sig_right, a.sig_seq);
+}
+
 __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
     if (__any_sync(__activemask(), bad) && bad) atomicOr(flag, 1);
 }
@@ -81,6 +99,8 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_len_c
     bool bad = false;
     for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * kClassicB; i0 < a.N; i0 += (std::uint64_t)gridDim.x * kClassicB) {
         const int nb = (int)min((std::uint64_t)kClassicB, a.N - i0);
+        const bool lb = i0 == 0, rb = i0 + nb == a.N; // boundary blocks read / feed the neighbours
+        classic_round_wait(a, lb, rb);
         if (KIND & 1) {
             const int s = (KIND == 1) ? 0 : 3;
             for (int t = threadIdx.x; t < nb + 2; t += blockDim.x) {
@@ -119,6 +139,7 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_len_c
             }
         }
         __syncthreads();
+        classic_round_signal(a, lb, rb);
     }
     raise_flag(a.error_flag, bad);
 }
@@ -135,6 +156,8 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_flat_
     bool bad = false;
     for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * kClassicB; i0 < a.N; i0 += (std::uint64_t)gridDim.x * kClassicB) {
         const int nb = (int)min((std::uint64_t)kClassicB, a.N - i0);
+        const bool lb = i0 == 0, rb = i0 + nb == a.N;
+        classic_round_wait(a, lb, rb);
         for (int t = threadIdx.x; t < nb + 4; t += blockDim.x) { // sp[t] = p(i0 + t - 2)
             const std::int64_t x = (std::int64_t)i0 + t - 2;
             sp[t] = em::pressure(F.ld(s, x), F.ld(s + 1, x), F.ld(s + 2, x), gamma, bad);
@@ -161,6 +184,7 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_flat_
             if (a.dbg.cov) classic_count(a, x);
         }
         __syncthreads();
+        classic_round_signal(a, lb, rb);
     }
     raise_flag(a.error_flag, bad);
 }

@@ -42,17 +42,29 @@ __device__ __forceinline__ double heat_f(double l, double c, double r, double fo
 }
 
 __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) {
-    // Two points per thread (N is a multiple of the even block width).
+    // Two points per thread (N is a multiple of the even block width). Only the
+    // threads owning points 0 and N-1 touch the neighbours: they wait for the
+    // neighbour's previous round (one process per GPU), read the halo, and
+    // signal this round once their boundary value is stored.
     const std::uint64_t pairs = a.N >> 1;
     const double fo = a.fourier;
-    const double hl = *a.halo_l;
-    const double hr = *a.halo_r;
     for (std::uint64_t p = blockIdx.x * (std::uint64_t)blockDim.x + threadIdx.x; p < pairs;
          p += (std::uint64_t)gridDim.x * blockDim.x) {
         const std::uint64_t i = p << 1;
         const double2 c = __ldg(reinterpret_cast<const double2*>(a.in) + p);
-        const double l = i > 0 ? __ldg(a.in + i - 1) : hl;
-        const double r = i + 2 < a.N ? __ldg(a.in + i + 2) : hr;
+        double l, r;
+        if (i > 0) {
+            l = __ldg(a.in + i - 1);
+        } else {
+            if (a.nb_flags) flag_wait(a.nb_flags, a.wait_seq, a.error_flag, a.timeout_ns);
+            l = *a.halo_l;
+        }
+        if (i + 2 < a.N) {
+            r = __ldg(a.in + i + 2);
+        } else {
+            if (a.nb_flags) flag_wait(a.nb_flags + 1, a.wait_seq, a.error_flag, a.timeout_ns);
+            r = *a.halo_r;
+        }
         double2 o;
         o.x = heat_f(l, c.x, c.y, fo);
         o.y = heat_f(c.x, c.y, r, fo);
@@ -63,6 +75,10 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
             atomicAdd(row + (a.dbg.gstart + i + 1) % a.dbg.cov_n, 1u);
         }
         reinterpret_cast<double2*>(a.out)[p] = o;
+        if (a.nb_flags) {
+            if (i == 0) flag_signal(a.sig_left, a.sig_seq);
+            if (i + 2 >= a.N) flag_signal(a.sig_right, a.sig_seq);
+        }
     }
 }
 

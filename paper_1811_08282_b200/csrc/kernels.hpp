@@ -67,6 +67,17 @@ struct ClassicArgs {
     double fourier = 0.4, gamma = 1.4, dt_dx = 0.0;
     int* error_flag = nullptr;
     DebugArgs dbg;
+    // One process per GPU: the round's neighbour hand-off is fused into the
+    // substep kernel. nb_flags[0]/[1] = rounds completed by the left/right
+    // neighbour (this shard's memory); the boundary points wait for wait_seq
+    // there before reading the halo and, once written, store sig_seq into the
+    // left neighbour's [1] (sig_left) and the right neighbour's [0] (sig_right).
+    // nb_flags == nullptr: no hand-off (single process / one shard).
+    const unsigned* nb_flags = nullptr;
+    unsigned wait_seq = 0, sig_seq = 0;
+    unsigned* sig_left = nullptr;
+    unsigned* sig_right = nullptr;
+    unsigned long long timeout_ns = 0;
 };
 
 // `debug` selects the instrumented instantiation (coverage / perturb).
