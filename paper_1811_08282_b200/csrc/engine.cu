@@ -15,6 +15,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -105,10 +106,25 @@ struct Solver {
     PipeIO* pio = nullptr;
     std::string last_error;
     std::vector<double> host_ic; // initial condition of the local shards (global order within)
+    // Single-shard classic substep loops are launch-bound on small grids: the
+    // loop is captured once into a CUDA graph and replayed (S1D_NO_GRAPHS=1
+    // disables it). Keyed by the counter range and the starting buffer; the
+    // dominant-kernel events are recorded around the graph launch.
+    struct ClassicGraph {
+        std::int64_t c0 = 0, c1 = -1;
+        const double* start = nullptr;
+        int end_idx = 0;
+        std::uint64_t launches = 0;
+        cudaGraphExec_t exec = nullptr;
+    } cgraph;
 
     ~Solver() { release(); }
 
     void release() {
+        if (cgraph.exec) {
+            cudaGraphExecDestroy(cgraph.exec);
+            cgraph.exec = nullptr;
+        }
         for (auto& s : shards) {
             if (!s.local) continue;
             cudaSetDevice(s.dev);
@@ -497,6 +513,46 @@ struct Solver {
 
     void classic_steps(std::int64_t c_begin, std::int64_t c_end, std::vector<const double*>& cur, int* cur_idx,
                        s1d_stats& stats, bool dominant = false) {
+        static const bool no_graphs = [] {
+            const char* e = std::getenv("S1D_NO_GRAPHS");
+            return e && e[0] == '1';
+        }();
+        if (R() == 1 && !debug && !no_graphs && c_begin <= c_end) {
+            Shard& s = sh(locals[0]);
+            S1D_CUDA(cudaSetDevice(s.dev));
+            const double* start = cur[0];
+            if (!(cgraph.exec && cgraph.c0 == c_begin && cgraph.c1 == c_end && cgraph.start == start)) {
+                if (cgraph.exec) S1D_CUDA(cudaGraphExecDestroy(cgraph.exec));
+                cgraph.exec = nullptr;
+                std::vector<const double*> cc = cur;
+                int idx = *cur_idx;
+                s1d_stats tmp{};
+                S1D_CUDA(cudaStreamBeginCapture(s.st, cudaStreamCaptureModeThreadLocal));
+                classic_launches(c_begin, c_end, cc, &idx, tmp, false);
+                cudaGraph_t graph = nullptr;
+                S1D_CUDA(cudaStreamEndCapture(s.st, &graph));
+                const cudaError_t ie = cudaGraphInstantiate(&cgraph.exec, graph, 0);
+                cudaGraphDestroy(graph);
+                S1D_CUDA(ie);
+                cgraph.c0 = c_begin;
+                cgraph.c1 = c_end;
+                cgraph.start = start;
+                cgraph.end_idx = idx;
+                cgraph.launches = tmp.kernel_launches;
+            }
+            if (dominant) record_all(&Shard::ev_dom0);
+            S1D_CUDA(cudaGraphLaunch(cgraph.exec, s.st));
+            if (dominant) record_all(&Shard::ev_dom1);
+            stats.kernel_launches += cgraph.launches;
+            *cur_idx = cgraph.end_idx;
+            cur[0] = s.state[cgraph.end_idx];
+            return;
+        }
+        classic_launches(c_begin, c_end, cur, cur_idx, stats, dominant);
+    }
+
+    void classic_launches(std::int64_t c_begin, std::int64_t c_end, std::vector<const double*>& cur, int* cur_idx,
+                          s1d_stats& stats, bool dominant) {
         // cur[g]: buffer holding shard g's current level; heat ping-pongs
         // through state[0]/state[1] (cur_idx: which one holds the result, -1 =
         // ic); Euler updates state[0] in place.
