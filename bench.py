@@ -39,6 +39,25 @@ HEAT_FLOPS_PER_UPDATE = 5  # heat_step: 2 DMUL + 3 DADD (inc/kernels.hpp:14-16)
 CLASSIC_BYTES_PER_UPDATE = 16  # one FP64 load + one store per point-update
 
 
+def euler_pipe_profile():
+    """FP64-pipe utilisation of the Euler swept Diamond (both methods) from the
+    committed ncu capture of this configuration (profiles/r01_euler_top_kernel.txt):
+    the Euler kernels are FP64-pipe bound (div/sqrt-heavy fluxes)."""
+    path = os.path.join(ROOT, "profiles", "r01_euler_top_kernel.txt")
+    out = {"bound": "fp64", "kernel": "euler_tile (swept Diamond)", "unit": "% of FP64 pipe cycles",
+           "source": "ncu sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active, " + os.path.relpath(path, ROOT)}
+    try:
+        method = None
+        for line in open(path):
+            if line.startswith("== ") and "euler_tile<" in line:
+                method = "flattening" if "euler_tile<1" in line else "lengthening"
+            elif method and "sm__pipe_fp64_cycles_active" in line:
+                out[f"{method}_fp64_pipe_active_pct"] = float(line.split()[1])
+    except OSError:
+        return None
+    return out
+
+
 def env_int(name, default):
     try:
         return int(os.environ.get(name, default))
@@ -319,6 +338,7 @@ def run_b200(args, rank, world):
                     best = min(es.advance()[1].loop_seconds for _ in range(2))
                 euler[f"{meth}_{sch}"] = round(ecfg.grid_size * ecfg.steps / best / 1e6, 2)
             euler[f"{meth}_swept_speedup"] = round(euler[f"{meth}_swept"] / euler[f"{meth}_classic"], 3)
+        euler["roofline"] = euler_pipe_profile()
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
