@@ -516,13 +516,17 @@ struct Solver {
             const char* e = std::getenv("S1D_NO_GRAPHS");
             return e && e[0] == '1';
         }();
-        return R() == 1 && !debug && !no_graphs;
+        // one local shard: a single process (one GPU) or one process per GPU
+        // (fused hand-off); single-process multi-device rounds use events
+        return locals.size() == 1 && (R() == 1 || mp) && !debug && !no_graphs;
     }
+    bool fused_rounds() const { return mp && R() > 1; }
     // Capture (once) the classic loop over counters [c0, c1] starting from
-    // cur with ping-pong index idx. Called before the timed region so only the
-    // replay is timed.
+    // cur (all shards) with ping-pong index idx. Called before the timed
+    // region so only the replay is timed.
     void ensure_classic_graph(std::int64_t c0, std::int64_t c1, const std::vector<const double*>& cur, int idx) {
-        if (cgraph.exec && cgraph.c0 == c0 && cgraph.c1 == c1 && cgraph.start == cur[0]) return;
+        const double* start = cur[static_cast<std::size_t>(locals[0])];
+        if (cgraph.exec && cgraph.c0 == c0 && cgraph.c1 == c1 && cgraph.start == start) return;
         Shard& s = sh(locals[0]);
         S1D_CUDA(cudaSetDevice(s.dev));
         if (cgraph.exec) S1D_CUDA(cudaGraphExecDestroy(cgraph.exec));
@@ -539,14 +543,30 @@ struct Solver {
         S1D_CUDA(cudaGraphUpload(cgraph.exec, s.st)); // first launch then replays only
         cgraph.c0 = c0;
         cgraph.c1 = c1;
-        cgraph.start = cur[0];
+        cgraph.start = start;
         cgraph.end_idx = idx;
         cgraph.launches = tmp.kernel_launches;
     }
 
     void classic_steps(std::int64_t c_begin, std::int64_t c_end, std::vector<const double*>& cur, int* cur_idx,
                        s1d_stats& stats, bool dominant = false) {
-        if (use_classic_graph() && c_begin <= c_end) {
+        if (c_begin > c_end) return;
+        const bool fused = fused_rounds();
+        if (fused) {
+            // One process per GPU: the round's hand-off is fused into the
+            // substep kernel (its boundary points wait / signal, kernels.hpp
+            // ClassicArgs), one launch per round. The previous round may have
+            // written into this shard's state from a neighbour (a seam-centred
+            // DownTriangle spills its right half into the right shard's array;
+            // the pad runs right after it), and interior points do not wait in
+            // a fused round: one full wait first. Then the rounds' sequence
+            // base goes to device memory (flags[2]).
+            wait_neighbours();
+            Shard& s = sh(locals[0]);
+            S1D_CUDA(cudaSetDevice(s.dev));
+            S1D_CUDA(launch_set_u32(s.flags + 2, seq, s.st));
+        }
+        if (use_classic_graph()) {
             Shard& s = sh(locals[0]);
             S1D_CUDA(cudaSetDevice(s.dev));
             ensure_classic_graph(c_begin, c_end, cur, *cur_idx);
@@ -555,10 +575,11 @@ struct Solver {
             if (dominant) record_all(&Shard::ev_dom1);
             stats.kernel_launches += cgraph.launches;
             *cur_idx = cgraph.end_idx;
-            cur[0] = s.state[cgraph.end_idx];
-            return;
+            for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).state[cgraph.end_idx];
+        } else {
+            classic_launches(c_begin, c_end, cur, cur_idx, stats, dominant);
         }
-        classic_launches(c_begin, c_end, cur, cur_idx, stats, dominant);
+        if (fused) seq += static_cast<unsigned>(c_end - c_begin + 1);
     }
 
     void classic_launches(std::int64_t c_begin, std::int64_t c_end, std::vector<const double*>& cur, int* cur_idx,
@@ -566,15 +587,7 @@ struct Solver {
         // cur[g]: buffer holding shard g's current level; heat ping-pongs
         // through state[0]/state[1] (cur_idx: which one holds the result, -1 =
         // ic); Euler updates state[0] in place.
-        // One process per GPU: the round's hand-off is fused into the substep
-        // kernel (its boundary points wait / signal, kernels.hpp ClassicArgs),
-        // one launch per round instead of wait + substep + signal.
-        const bool fused = mp && R() > 1;
-        // The previous round may have written into this shard's state from a
-        // neighbour (a seam-centred DownTriangle spills its right half into the
-        // right shard's array; the pad runs right after it), and interior
-        // points do not wait in a fused round: one full wait first.
-        if (fused && c_begin <= c_end) wait_neighbours();
+        const bool fused = fused_rounds();
         for (std::int64_t c = c_begin; c <= c_end; ++c) {
             if (!fused) wait_neighbours();
             if (dominant && c == c_begin) record_all(&Shard::ev_dom0);
@@ -603,8 +616,8 @@ struct Solver {
                 a.dbg = dbg_args(g);
                 if (fused) {
                     a.nb_flags = s.flags;
-                    a.wait_seq = seq;
-                    a.sig_seq = seq + 1;
+                    a.seq_base = s.flags + 2;
+                    a.round = static_cast<unsigned>(c - c_begin);
                     a.sig_left = L.flags + 1; // I am my left neighbour's right neighbour
                     a.sig_right = Rt.flags + 0;
                     a.timeout_ns = kRoundTimeoutNs;
@@ -615,8 +628,7 @@ struct Solver {
                 stats.kernel_launches += 1;
             }
             if (dominant && c == c_end) record_all(&Shard::ev_dom1);
-            if (fused) ++seq;
-            else record_round();
+            if (!fused) record_round();
             *cur_idx = nxt;
             for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).state[nxt];
         }
@@ -708,7 +720,8 @@ struct Solver {
 
         if (pad > 0 && use_classic_graph()) { // capture outside the timed region
             const bool from_state = cycles >= 1 || euler;
-            std::vector<const double*> c0(1, from_state ? sh(locals[0]).state[0] : sh(locals[0]).ic);
+            std::vector<const double*> c0(static_cast<std::size_t>(R()));
+            for (int g = 0; g < R(); ++g) c0[static_cast<std::size_t>(g)] = from_state ? sh(g).state[0] : sh(g).ic;
             ensure_classic_graph(cycles * static_cast<std::int64_t>(m) + 1, total, c0, from_state ? 0 : -1);
         }
         sync_all();

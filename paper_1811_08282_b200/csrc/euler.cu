@@ -72,15 +72,17 @@ __device__ __forceinline__ void classic_count(const ClassicArgs& a, std::uint64_
 __device__ __forceinline__ void classic_round_wait(const ClassicArgs& a, bool lb, bool rb) {
     if (!a.nb_flags || !(lb || rb)) return;
     if (threadIdx.x == 0) {
-        if (lb) flag_wait(a.nb_flags, a.wait_seq, a.error_flag, a.timeout_ns);
-        if (rb) flag_wait(a.nb_flags + 1, a.wait_seq, a.error_flag, a.timeout_ns);
+        const unsigned seq = *a.seq_base + a.round;
+        if (lb) flag_wait(a.nb_flags, seq, a.error_flag, a.timeout_ns);
+        if (rb) flag_wait(a.nb_flags + 1, seq, a.error_flag, a.timeout_ns);
     }
     __syncthreads();
 }
 __device__ __forceinline__ void classic_round_signal(const ClassicArgs& a, bool lb, bool rb) {
     if (!a.nb_flags || threadIdx.x != 0) return;
-    if (lb) flag_signal(a.sig_left, a.sig_seq);
-    if (rb) flag_signal(a.sig_right, a.sig_seq);
+    const unsigned seq = *a.seq_base + a.round + 1;
+    if (lb) flag_signal(a.sig_left, seq);
+    if (rb) flag_signal(a.sig_right, seq);
 }
 
 __device__ __forceinline__ void raise_flag(int* flag, bool bad) {

@@ -56,13 +56,13 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
         if (i > 0) {
             l = __ldg(a.in + i - 1);
         } else {
-            if (a.nb_flags) flag_wait(a.nb_flags, a.wait_seq, a.error_flag, a.timeout_ns);
+            if (a.nb_flags) flag_wait(a.nb_flags, *a.seq_base + a.round, a.error_flag, a.timeout_ns);
             l = *a.halo_l;
         }
         if (i + 2 < a.N) {
             r = __ldg(a.in + i + 2);
         } else {
-            if (a.nb_flags) flag_wait(a.nb_flags + 1, a.wait_seq, a.error_flag, a.timeout_ns);
+            if (a.nb_flags) flag_wait(a.nb_flags + 1, *a.seq_base + a.round, a.error_flag, a.timeout_ns);
             r = *a.halo_r;
         }
         double2 o;
@@ -76,8 +76,8 @@ __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) 
         }
         reinterpret_cast<double2*>(a.out)[p] = o;
         if (a.nb_flags) {
-            if (i == 0) flag_signal(a.sig_left, a.sig_seq);
-            if (i + 2 >= a.N) flag_signal(a.sig_right, a.sig_seq);
+            if (i == 0) flag_signal(a.sig_left, *a.seq_base + a.round + 1);
+            if (i + 2 >= a.N) flag_signal(a.sig_right, *a.seq_base + a.round + 1);
         }
     }
 }

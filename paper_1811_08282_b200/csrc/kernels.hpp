@@ -69,12 +69,15 @@ struct ClassicArgs {
     DebugArgs dbg;
     // One process per GPU: the round's neighbour hand-off is fused into the
     // substep kernel. nb_flags[0]/[1] = rounds completed by the left/right
-    // neighbour (this shard's memory); the boundary points wait for wait_seq
-    // there before reading the halo and, once written, store sig_seq into the
-    // left neighbour's [1] (sig_left) and the right neighbour's [0] (sig_right).
-    // nb_flags == nullptr: no hand-off (single process / one shard).
+    // neighbour (this shard's memory); the boundary points wait for
+    // *seq_base + round there before reading the halo and, once written, store
+    // *seq_base + round + 1 into the left neighbour's [1] (sig_left) and the
+    // right neighbour's [0] (sig_right). seq_base (device memory, set before
+    // the rounds) keeps the kernel arguments constant across runs, so the round
+    // loop can be replayed as a CUDA graph. nb_flags == nullptr: no hand-off.
     const unsigned* nb_flags = nullptr;
-    unsigned wait_seq = 0, sig_seq = 0;
+    const unsigned* seq_base = nullptr;
+    unsigned round = 0;
     unsigned* sig_left = nullptr;
     unsigned* sig_right = nullptr;
     unsigned long long timeout_ns = 0;
@@ -101,6 +104,7 @@ std::size_t euler_tile_smem_bytes(int flat, int w);
 cudaError_t launch_wait_flags(const unsigned* flags, unsigned seq, int* err, std::uint64_t timeout_ns,
                               cudaStream_t st);
 cudaError_t launch_signal_flags(unsigned* left_slot, unsigned* right_slot, unsigned seq, cudaStream_t st);
+cudaError_t launch_set_u32(unsigned* p, unsigned v, cudaStream_t st);
 cudaError_t launch_pingpong(const unsigned* mine, unsigned* peer, int iters, int starter, int* err,
                             std::uint64_t timeout_ns, cudaStream_t st);
 

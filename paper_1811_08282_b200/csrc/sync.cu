@@ -76,7 +76,14 @@ __global__ void pingpong_kernel(const unsigned* mine, unsigned* peer, int iters,
     }
 }
 
+__global__ void set_u32_kernel(unsigned* p, unsigned v) { *p = v; }
+
 } // namespace
+
+cudaError_t launch_set_u32(unsigned* p, unsigned v, cudaStream_t st) {
+    set_u32_kernel<<<1, 1, 0, st>>>(p, v);
+    return cudaGetLastError();
+}
 
 cudaError_t launch_pingpong(const unsigned* mine, unsigned* peer, int iters, int starter, int* err,
                             std::uint64_t timeout_ns, cudaStream_t st) {
