@@ -115,3 +115,22 @@ def test_euler_2p22_swept_classic_flat_len_agree(euler_len_swept):
     spec = s1d.make_spec(s1d.Equation.Euler, s1d.Method.Lengthening)
     ic = s1d.initial_condition("euler-sod-periodic", 1 << 22, spec).reshape(-1, 3)
     assert abs(rho.sum() - ic[:, 0].sum()) <= 1e-12 * ic[:, 0].sum()
+
+
+@pytest.mark.parametrize("method", [s1d.Method.Lengthening, s1d.Method.Flattening], ids=["len", "flat"])
+def test_euler_2p26_windows_match_oracle(gpu, method):
+    # the top of BASELINE configs[2] (n = 2^20 .. 2^26); windows across both Sod jumps
+    n, T = 1 << 26, 256
+    cfg = s1d.LaunchConfig(equation=s1d.Equation.Euler, method=method, scheme=s1d.Scheme.Swept, grid_size=n,
+                           block_width=512, ranks=1, steps=T, mode=s1d.Mode.WallClock)
+    got = s1d.run(cfg).state.reshape(-1, 3)
+    cfg.finalize()
+    spec = s1d.make_spec(s1d.Equation.Euler, s1d.Method.Lengthening)
+    name = "lengthening" if method == s1d.Method.Lengthening else "flattening"
+    pad, W = 4 * T + 8, 64
+    for x0 in (-32, n // 2 - 32):
+        idx = np.arange(x0 - pad, x0 + W + pad) % n
+        ic = np.concatenate([s1d.initial_condition_range("euler-sod-periodic", n, spec, a, b - a)
+                             for a, b in ((int(idx[i]), int(idx[j - 1]) + 1) for i, j in _runs(idx))])
+        want = O.port_run_state("euler", name, ic, T, cfg.phys.dt_dx).reshape(-1, 3)[pad:pad + W]
+        assert np.array_equal(bits(got[np.arange(x0, x0 + W) % n]), bits(want))
