@@ -964,7 +964,7 @@ int guarded_solver(s1d_solver* s, Fn&& fn) {
 
 extern "C" {
 
-const char* s1d_version(void) { return "swept1d-b200 0.1.0 (sm_100a, FP64)"; }
+const char* s1d_version(void) { return "swept1d-b200 0.2.0 (sm_100a, FP64)"; }
 int s1d_abi_version(void) { return S1D_ABI_VERSION; }
 
 int s1d_device_count(void) {
