@@ -130,10 +130,16 @@ __device__ __forceinline__ void cp_async8(double* smem_dst, const double* gsrc) 
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(d), "l"(gsrc) : "memory");
 }
 
-// Production rings hold min(kRing, pow2ceil(m)) levels (short tiles need no
-// more), so narrow tiles keep shared memory — and occupancy — small.
+#ifndef S1D_HEAT_XPORT_LEVELS
+#define S1D_HEAT_XPORT_LEVELS 32
+#endif
+constexpr int kXportLevels = S1D_HEAT_XPORT_LEVELS; // short tiles (XS builds): m <= this (w <= 64)
+
+// Production rings hold pow2ceil(m) levels for short tiles (the whole edge,
+// loaded at once; their shared-memory region is sized by the staged exports
+// anyway) and kRing levels, streamed, for longer ones.
 __host__ __device__ inline int ring_levels(int m) {
-    if (m >= kRing) return kRing;
+    if (m > kXportLevels) return kRing;
     int l = 1;
     while (l < m) l *= 2;
     return l;
@@ -282,11 +288,6 @@ __device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], dou
     fcontract_seg<Q, U, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
 }
 
-#ifndef S1D_HEAT_XPORT_LEVELS
-#define S1D_HEAT_XPORT_LEVELS 32
-#endif
-constexpr int kXportLevels = S1D_HEAT_XPORT_LEVELS; // stage exports for m <= this (w <= 64)
-
 // Shared memory (doubles): exchange 8*(tt+2)*G, then one region reused in turn:
 // ring 4*levels*G (Diamond/Down), state staging G*(w+1) (Up/Down) and, for
 // short tiles, export staging 2*G*(w+1) (Up/Diamond, after the last ring read).
@@ -372,18 +373,18 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     };
     const double* pR = nullptr;
     const double* pL = nullptr;
-    const bool feeder = live && s == 0 && KIND != kUp && m > kRing;
+    const bool feeder = live && s == 0 && KIND != kUp && m > rl;
     if (KIND != kUp) {
         if (live) {
             pR = srcR(b);
             pL = srcL(b);
         }
-        // Levels 1..min(m, kRing), whole CTA, coalesced per tile. Short tiles
+        // Levels 1..min(m, rl), whole CTA, coalesced per tile. Short tiles
         // (the whole edge fits the ring) use cp.async so all of a thread's
         // loads are in flight at once (measured: +10% at w = 32, -2.6% at
         // w = 1024, where plain loads win).
-        const int n0 = 2 * (m < kRing ? m : kRing);
-        if (XS && m <= kRing) {
+        const int n0 = 2 * (m < rl ? m : rl);
+        if (XS) {
             for (int j = t; j < ntiles * n0; j += nt) {
                 const int gg = j / n0, i = j - gg * n0;
                 cp_async8(ringR + ridx(i, rmask, gg, G), srcR(bfirst + gg) + i);
