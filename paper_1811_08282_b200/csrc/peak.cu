@@ -39,6 +39,17 @@ extern "C" int s1d_measure_fp64_peak(int device, double* ops_per_second, char* e
         }
         return (int)S1D_CUDA_ERROR;
     };
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+        cudaGetLastError();
+        if (err && errlen) {
+            const std::string m = "no CUDA device visible";
+            const size_t n = m.size() < errlen - 1 ? m.size() : errlen - 1;
+            m.copy(err, n);
+            err[n] = 0;
+        }
+        return (int)S1D_NO_DEVICE;
+    }
     cudaError_t e = cudaSetDevice(device);
     if (e != cudaSuccess) return fail("cudaSetDevice", e);
     int sms = 0;

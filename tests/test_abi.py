@@ -54,6 +54,13 @@ def test_no_cpu_fallback_without_gpu():
         s1d.run(s1d.LaunchConfig(grid_size=64, block_width=8, steps=2))
     with pytest.raises(s1d.NoDevice):
         s1d.Solver(s1d.LaunchConfig(grid_size=64, block_width=8, steps=2))
+    with pytest.raises(s1d.NoDevice):
+        s1d.calibrate_transport(0, 1)
+    with pytest.raises(s1d.NoDevice):
+        s1d.measure_fp64_peak(0)
+    # the virtual-time model is host-only and works without a GPU
+    v, comm = s1d.virtual_time(s1d.LaunchConfig(grid_size=64, block_width=8, steps=2))
+    assert v > 0 and comm == 0.0
 
 
 def test_defaults_mirror_reference():
