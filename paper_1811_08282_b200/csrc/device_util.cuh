@@ -12,6 +12,21 @@ __device__ __forceinline__ double next_up(double x) {
     return __longlong_as_double(x > 0.0 ? b + 1 : b - 1);
 }
 
+// Checked builds (-DS1D_CHECKED): index bounds of the tile kernels' shared
+// and global accesses are verified at run time; a violation sets bit 2 (value
+// 4) of the launch's error flag (no trap, so the GPU never needs a reset) and
+// the host reports S1D_INTERNAL.
+#ifdef S1D_CHECKED
+#define S1D_CHECK(cond, flag)                                                                                      \
+    do {                                                                                                           \
+        if (!(cond)) atomicOr((flag), 4);                                                                          \
+    } while (0)
+#else
+#define S1D_CHECK(cond, flag)                                                                                      \
+    do {                                                                                                           \
+    } while (0)
+#endif
+
 // Round hand-off between shards of different processes (one process per GPU):
 // a shard's flag word holds the rounds completed by one ring neighbour, stored
 // by that neighbour over NVLink (system-scope release) and polled here

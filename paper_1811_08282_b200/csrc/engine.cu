@@ -807,6 +807,7 @@ struct Solver {
             s.final_state = cur[static_cast<std::size_t>(g)];
         }
         S1D_CUDA(cudaGetLastError());
+        if (flag & 4) throw Error(S1D_INTERNAL, "device bounds check failed (checked build)");
         if (flag & 2) throw Error(S1D_TRANSPORT_ABORTED, "a neighbour shard stopped responding (round timeout)");
         if (flag) throw Error(S1D_NONPHYSICAL, "non-physical state encountered on the device");
 

@@ -287,6 +287,7 @@ __global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1 : S1D_EULER_MINB) euler_t
     auto for_all = [&](int x0, int x1, auto&& f) {
         const int cnt = x1 - x0;
         if (cnt <= 0) return;
+        S1D_CHECK(x0 >= 0 && x1 <= W2, a.error_flag); // phase ranges stay inside the tile's records
         if (GT == 1) {
             if (live(0))
                 for (int x = x0 + t; x < x1; x += NT) f(0, x);
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1 : S1D_EULER_MINB) euler_t
             if (!live(gi)) continue;
             const int side = k / LVL, j = k % LVL, rec = j / REC, f = j % REC;
             const int x = side == 0 ? lo - H + rec : hi - H + rec;
+            S1D_CHECK(x >= 0 && x < W2, a.error_flag);
             S(gi)[f * W2 + x] = ring(gi)[((std::size_t)side * kERing + (q - 1) % kERing) * LVL + j];
         }
     };
@@ -450,6 +452,7 @@ __global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1 : S1D_EULER_MINB) euler_t
             const int b = tile_of(gi);
             const int side = k / LVL, j = k % LVL, rec = j / REC, f = j % REC;
             const int x = side == 0 ? lo + rec : hi - 2 * H + rec;
+            S1D_CHECK(x >= 0 && x < W2 && d >= 0 && d < m, a.error_flag);
             double* o = (side == 0 ? a.out_L : a.out_R) + (std::size_t)b * tstride + (std::size_t)d * LVL;
             o[j] = S(gi)[f * W2 + x];
         }

@@ -160,6 +160,7 @@ struct Fold {
     double2* Lst;        // [2][(tt+2)G]: (vl[Q-1], vr[Q-1]) of slot s at (s+1)G+g
     int xs;              // parity stride (double2 elements)
     int rmask;           // ring index mask
+    int* err;            // launch error flag (checked builds: bounds violations)
     const double* ringR; // left producer's R edges
     const double* ringL; // right producer's L edges
 };
@@ -167,6 +168,7 @@ struct Fold {
 template <int Q>
 __device__ __forceinline__ void fpublish(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int r) {
     const int i = (r & 1) * c.xs + (c.s + 1) * c.G + c.g;
+    S1D_CHECK(i >= 0 && i < 2 * c.xs, c.err);
     c.F[i] = make_double2(vl[0], vr[0]);
     c.Lst[i] = make_double2(vl[Q - 1], vr[Q - 1]);
 }
@@ -176,6 +178,7 @@ __device__ __forceinline__ void fcompute(const Fold<Q>& c, double (&vl)[Q], doub
     const int par = (r & 1) * c.xs;
     const double2 in = c.Lst[par + c.s * c.G + c.g];      // slot s-1: distance sQ-1
     const double2 out = c.F[par + (c.s + 2) * c.G + c.g]; // slot s+1: distance sQ+Q
+    S1D_CHECK(par + (c.s + 2) * c.G + c.g < 2 * c.xs, c.err);
     const double inL = c.s == 0 ? vr[0] : in.x;           // x+1 of left distance sQ
     const double inR = c.s == 0 ? vl[0] : in.y;           // x-1 of right distance sQ
     double nl[Q], nr[Q];
@@ -203,6 +206,9 @@ __device__ __forceinline__ void finsert(const Fold<Q>& c, double (&vl)[Q], doubl
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         if (d0 + k >= r - 1) {
+            S1D_CHECK(ridx(3 * r - 2 - d0 - k, c.rmask, c.g, c.G) < (c.rmask + 1) * c.G &&
+                          ridx(r - 1 + d0 + k, c.rmask, c.g, c.G) < (c.rmask + 1) * c.G,
+                      c.err);
             vl[k] = c.ringR[ridx(3 * r - 2 - d0 - k, c.rmask, c.g, c.G)];
             vr[k] = c.ringL[ridx(r - 1 + d0 + k, c.rmask, c.g, c.G)];
         }
@@ -214,6 +220,7 @@ template <int Q>
 __device__ __forceinline__ void fexport(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int d,
                                         double* oL, double* oR, bool live) {
     const int d0 = c.s * Q, e1 = c.m - 1 - d, e2 = c.m - 2 - d;
+    S1D_CHECK(d >= 0 && d < c.m, c.err); // edge slots 2d, 2d+1 of the tile's w = 2m
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         if (live && d0 + k == e1) {
@@ -332,6 +339,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     const int rl = ring_levels(m);
     const int rmask = 2 * rl - 1;
     c.rmask = rmask;
+    c.err = a.error_flag;
     double* const ringR = sm + 8 * c.xs; // [2*rl][G]
     double* const ringL = ringR + 2 * rl * G;
     double* const stage = ringR;         // Up/Down [G][w+1]
@@ -387,6 +395,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         if (XS) {
             for (int j = t; j < ntiles * n0; j += nt) {
                 const int gg = j / n0, i = j - gg * n0;
+                S1D_CHECK(i < 2 * m && ridx(i, rmask, gg, G) < 2 * rl * G, a.error_flag);
                 cp_async8(ringR + ridx(i, rmask, gg, G), srcR(bfirst + gg) + i);
                 cp_async8(ringL + ridx(i, rmask, gg, G), srcL(bfirst + gg) + i);
             }
@@ -408,6 +417,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         if (feeder) {
             const int q = r + kRing - 2; // 0-based index of level r+kRing-1
             if (q < m) {
+                S1D_CHECK(2 * q + 1 < w && ridx(2 * q + 1, rmask, g, G) < 2 * rl * G, a.error_flag);
                 cp_async8(ringR + ridx(2 * q, rmask, g, G), pR + 2 * q);
                 cp_async8(ringR + ridx(2 * q + 1, rmask, g, G), pR + 2 * q + 1);
                 cp_async8(ringL + ridx(2 * q, rmask, g, G), pL + 2 * q);
@@ -472,6 +482,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
             const int gg = j / w;
             const double val = stage[gg * ws + (j - gg * w)];
             const std::uint64_t gp = (std::uint64_t)(p0 + j);
+            S1D_CHECK(gp < a.N + (std::uint64_t)w, a.error_flag); // spill into the right shard <= w/2
             if (gp < a.N) a.state_out[gp] = val;
             else a.state_right[gp - a.N] = val;
         }
