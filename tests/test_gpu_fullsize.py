@@ -1,6 +1,8 @@
 """GPU parity at the BASELINE sizes (configs 1-2), through size-independent
 properties — the CPU oracle cannot run 2^27 points x thousands of steps:
 
+  * heat n = 2^27: linear under power-of-two scaling (bitwise) and max-norm
+    non-increasing at Fo = 0.5 (test_kernels.cpp:43-74 at full size);
   * heat n = 2^27: swept (w = 1024 and the short-tile path, w = 32) ==
     classic, bit for bit; and windows of the result == an exact FTCS
     restatement run on the window's dependency cone (the value at x after T
@@ -134,3 +136,32 @@ def test_euler_2p26_windows_match_oracle(gpu, method):
                              for a, b in ((int(idx[i]), int(idx[j - 1]) + 1) for i, j in _runs(idx))])
         want = O.port_run_state("euler", name, ic, T, cfg.phys.dt_dx).reshape(-1, 3)[pad:pad + W]
         assert np.array_equal(bits(got[np.arange(x0, x0 + W) % n]), bits(want))
+
+
+def test_heat_2p27_linear_under_power_of_two_scaling(gpu):
+    # test_kernels.cpp:43-48 at full size: scaling the state by 2^k is exact,
+    # so solve(4 u0) == 4 solve(u0) bit for bit (swept, w = 1024)
+    cfg = s1d.LaunchConfig(equation=s1d.Equation.Heat, scheme=s1d.Scheme.Swept, grid_size=N_HEAT, block_width=1024,
+                           ranks=1, steps=T_HEAT, mode=s1d.Mode.WallClock)
+    u0 = s1d.initial_condition("heat-sine", N_HEAT, HEAT_SPEC)
+    with s1d.Solver(cfg) as sv:
+        a, _, _ = sv.solve(u0)
+        b, _, _ = sv.solve(4.0 * u0)
+    assert np.array_equal(bits(b), bits(4.0 * a))
+
+
+def test_heat_2p27_max_norm_non_increasing_at_fo_half(gpu):
+    # test_kernels.cpp:50-74 at full size: Fo = 0.5, rough data, max-norm
+    # non-increasing in T (swept)
+    x = np.arange(N_HEAT, dtype=np.float64)
+    u0 = np.sin(0.13 * x) + 0.2 * np.cos(0.41 * x * x)
+    prev = np.abs(u0).max()
+    for T in (64, 256, 1024):
+        cfg = s1d.LaunchConfig(equation=s1d.Equation.Heat, scheme=s1d.Scheme.Swept, grid_size=N_HEAT,
+                               block_width=1024, ranks=1, steps=T, mode=s1d.Mode.WallClock)
+        cfg.phys.fourier = 0.5
+        with s1d.Solver(cfg) as sv:
+            u, _, _ = sv.solve(u0)
+        cur = np.abs(u).max()
+        assert cur <= prev + 1e-15
+        prev = cur
