@@ -953,6 +953,11 @@ int guarded(char* err, size_t errlen, Fn&& fn) {
     }
 }
 
+// Null arguments fail loudly at the boundary (no dereference of a null config).
+void need(const void* p, const char* what) {
+    if (!p) throw s1d::Error(S1D_INVALID_CONFIG, std::string(what) + " is null");
+}
+
 template <class Fn>
 int guarded_solver(s1d_solver* s, Fn&& fn) {
     char buf[512];
@@ -999,15 +1004,20 @@ void s1d_config_defaults(s1d_config* c) {
 }
 
 int s1d_apply_config_entry(s1d_config* cfg, const char* key, const char* value, char* err, size_t errlen) {
-    return guarded(err, errlen, [&] { s1d::apply_config_entry(*cfg, key, value); });
+    return guarded(err, errlen, [&] {
+        need(cfg, "config");
+        need(key, "key");
+        need(value, "value"); s1d::apply_config_entry(*cfg, key, value); });
 }
 
 int s1d_validate(const s1d_config* cfg, int partitioned, char* err, size_t errlen) {
-    return guarded(err, errlen, [&] { s1d::validate(*cfg, partitioned != 0); });
+    return guarded(err, errlen, [&] {
+        need(cfg, "config"); s1d::validate(*cfg, partitioned != 0); });
 }
 
 int s1d_finalize(s1d_config* cfg, int partitioned, char* err, size_t errlen) {
-    return guarded(err, errlen, [&] { s1d::finalize(*cfg, partitioned != 0); });
+    return guarded(err, errlen, [&] {
+        need(cfg, "config"); s1d::finalize(*cfg, partitioned != 0); });
 }
 
 void s1d_spec(int equation, int method, int* substeps, int* half_width, int* slots, int* vpp) {
@@ -1044,6 +1054,7 @@ int s1d_max_signal_speed(const double* prim, size_t len, double gamma, double* o
 int s1d_partition(const s1d_config* cfg, uint64_t* blocks, uint64_t* start, int* left, int* right, char* err,
                   size_t errlen) {
     return guarded(err, errlen, [&] {
+        need(cfg, "config");
         const auto p = s1d::make_partition(*cfg);
         for (std::size_t r = 0; r < p.blocks.size(); ++r) {
             blocks[r] = p.blocks[r];
@@ -1063,6 +1074,7 @@ int64_t s1d_cycle_advance(uint64_t w, uint64_t h, char* err, size_t errlen) {
 int s1d_virtual_time(const s1d_config* cfg, double* virtual_seconds, double* comm_seconds, char* err,
                      size_t errlen) {
     return guarded(err, errlen, [&] {
+        need(cfg, "config");
         s1d_config c = *cfg;
         s1d::finalize(c, true);
         double comm = 0.0;
@@ -1186,6 +1198,8 @@ uint64_t s1d_swept_buffer_cells(uint64_t w, int equation, int method) {
 int s1d_run_debug(const s1d_config* cfg, const s1d_debug* dbg, double* state_out, size_t state_len, s1d_stats* stats,
                   s1d_timing* timing, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
+        need(cfg, "config");
+        need(state_out, "state_out");
         s1d::Solver solver;
         solver.init(*cfg);
         if (state_len < solver.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
@@ -1199,6 +1213,8 @@ int s1d_run_debug(const s1d_config* cfg, const s1d_debug* dbg, double* state_out
 
 int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
+        need(cfg, "config");
+        need(out, "record");
         s1d::Solver solver;
         solver.init(*cfg);
         s1d_stats st{};
@@ -1229,7 +1245,8 @@ int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen
 int s1d_create(const s1d_config* cfg, s1d_solver** out, char* err, size_t errlen) {
     *out = nullptr;
     auto holder = std::make_unique<s1d_solver>();
-    const int st = guarded(err, errlen, [&] { holder->impl.init(*cfg); });
+    const int st = guarded(err, errlen, [&] {
+        need(cfg, "config"); holder->impl.init(*cfg); });
     if (st == S1D_OK) *out = holder.release();
     return st;
 }
@@ -1286,7 +1303,8 @@ const char* s1d_last_error(const s1d_solver* s) { return s ? s->impl.last_error.
 int s1d_shard_create(const s1d_config* cfg, int rank, int device, s1d_solver** out, char* err, size_t errlen) {
     *out = nullptr;
     auto holder = std::make_unique<s1d_solver>();
-    const int st = guarded(err, errlen, [&] { holder->impl.init_shard(*cfg, rank, device); });
+    const int st = guarded(err, errlen, [&] {
+        need(cfg, "config"); holder->impl.init_shard(*cfg, rank, device); });
     if (st == S1D_OK) *out = holder.release();
     return st;
 }
@@ -1321,6 +1339,8 @@ int s1d_shard_range(const s1d_solver* s, uint64_t* start, uint64_t* count) {
 int s1d_run(const s1d_config* cfg, double* state_out, size_t state_len, s1d_stats* stats, s1d_timing* timing,
             char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
+        need(cfg, "config");
+        need(state_out, "state_out");
         s1d::Solver solver;
         solver.init(*cfg);
         if (state_len < solver.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");

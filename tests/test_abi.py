@@ -71,3 +71,13 @@ def test_defaults_mirror_reference():
     assert (c.grid_size, c.block_width, c.ranks, c.work_factor, c.steps) == (1024, 32, 2, 0, 50)
     assert (c.fourier, c.gamma, c.dt_dx, c.cfl, c.compute_cost) == (0.4, 1.4, 0.0, 0.4, 1e-8)
     assert c.scheme == int(d.scheme) == 1 and c.mode == int(d.mode) == 1
+
+
+def test_null_arguments_fail_loudly():
+    lib = _capi.lib()
+    e = C.create_string_buffer(256)
+    assert lib.s1d_validate(None, 1, e, 256) == 1 and b"null" in e.value
+    assert lib.s1d_run(None, None, 0, None, None, e, 256) == 1
+    assert lib.s1d_virtual_time(None, None, None, e, 256) == 1
+    h = C.c_void_p()
+    assert lib.s1d_create(None, C.byref(h), e, 256) == 1 and not h.value
