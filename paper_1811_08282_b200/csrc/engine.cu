@@ -1254,11 +1254,13 @@ int s1d_create(const s1d_config* cfg, s1d_solver** out, char* err, size_t errlen
 void s1d_destroy(s1d_solver* s) { delete s; }
 
 int s1d_get_config(const s1d_solver* s, s1d_config* out) {
+    if (!s) return S1D_INVALID_CONFIG;
     *out = s->impl.cfg;
     return S1D_OK;
 }
 
 int s1d_set_initial(s1d_solver* s, const double* host_state, size_t len) {
+    if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
         if (!host_state) {
             s->impl.upload(s->impl.host_ic.data(), s->impl.local_io());
@@ -1271,6 +1273,7 @@ int s1d_set_initial(s1d_solver* s, const double* host_state, size_t len) {
 }
 
 int s1d_advance(s1d_solver* s, s1d_stats* stats, s1d_timing* timing) {
+    if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
         if (timing) std::memset(timing, 0, sizeof(*timing));
         s->impl.advance(stats, timing);
@@ -1278,6 +1281,7 @@ int s1d_advance(s1d_solver* s, s1d_stats* stats, s1d_timing* timing) {
 }
 
 int s1d_read_state(s1d_solver* s, double* host_out, size_t len) {
+    if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
         if (len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
         for (int g : s->impl.locals)
@@ -1288,6 +1292,7 @@ int s1d_read_state(s1d_solver* s, double* host_out, size_t len) {
 
 int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_out, size_t out_len,
               s1d_stats* stats, s1d_timing* timing) {
+    if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
         if (host_in && in_len != s->impl.state_len())
             throw s1d::Error(S1D_INVALID_CONFIG, "initial state length mismatch");
@@ -1312,6 +1317,7 @@ int s1d_shard_create(const s1d_config* cfg, int rank, int device, s1d_solver** o
 size_t s1d_shard_blob_size(void) { return sizeof(s1d::ShardBlob); }
 
 int s1d_shard_export(s1d_solver* s, void* blob, size_t blob_len) {
+    if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
         if (blob_len < sizeof(s1d::ShardBlob)) throw s1d::Error(S1D_INVALID_CONFIG, "blob buffer too small");
         s->impl.export_blob(static_cast<s1d::ShardBlob*>(blob));
@@ -1319,12 +1325,14 @@ int s1d_shard_export(s1d_solver* s, void* blob, size_t blob_len) {
 }
 
 int s1d_shard_connect(s1d_solver* s, const void* left_blob, const void* right_blob) {
+    if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
         s->impl.connect(static_cast<const s1d::ShardBlob*>(left_blob), static_cast<const s1d::ShardBlob*>(right_blob));
     });
 }
 
 int s1d_shard_range(const s1d_solver* s, uint64_t* start, uint64_t* count) {
+    if (!s) return S1D_INVALID_CONFIG;
     if (s->impl.locals.size() != 1) {
         *start = 0;
         *count = s->impl.cfg.grid_size;

@@ -81,3 +81,4 @@ def test_null_arguments_fail_loudly():
     assert lib.s1d_virtual_time(None, None, None, e, 256) == 1
     h = C.c_void_p()
     assert lib.s1d_create(None, C.byref(h), e, 256) == 1 and not h.value
+    assert lib.s1d_advance(None, None, None) == 1 and lib.s1d_read_state(None, None, 0) == 1
