@@ -89,6 +89,16 @@ def test_long_run_conserves_mass(gpu):
 
 
 @pytest.mark.parametrize("method", ["lengthening", "flattening"])
+def test_20000_step_run_stays_physical_and_bitwise(gpu, method):
+    # Euler n=1024, 20000 steps, rho in [0.459, 0.632], mass to 5e-13
+    res = s1d.run(cfg(method, s1d.Scheme.Swept, 1024, 64, 20000))
+    rho = res.state[0::3]
+    assert 0.45 < rho.min() and rho.max() < 0.64
+    assert abs(rho.sum() - 576.0) <= 5e-13 * 576.0
+    assert_bitwise(res.state, O.port_run_serial("euler", method, n=1024, steps=20000))
+
+
+@pytest.mark.parametrize("method", ["lengthening", "flattening"])
 @pytest.mark.parametrize("scheme", SCHEMES, ids=s1d.to_string)
 def test_nonphysical_state_raises(gpu, method, scheme):
     # negative pressure somewhere inside the domain (test_kernels.cpp:251-255 at engine level)
