@@ -20,9 +20,11 @@
 // shared memory, one barrier, 5P FP64 ops from registers.
 //
 // Edges: the left producer's R edges and the right producer's L edges (2
-// values per level each) stream into a small shared-memory ring per tile
-// (cp.async, kRing-2 levels ahead); inserts reload the two entering
-// distances per side, exports store the two leaving ones.
+// values per level each) go through a shared-memory ring per tile. Short
+// tiles (m <= 32) load the whole edge at once with cp.async and stage their
+// exports for one coalesced write-back; longer tiles stream the ring
+// (cp.async, kLook levels ahead). Inserts reload the two entering distances
+// per side, exports store the two leaving ones.
 //
 // The instrumented debug kernel (heat_tile_debug_kernel) keeps an
 // independent contiguous layout (thread lt owns x = 1 + lt*P + k) with plain
