@@ -23,7 +23,7 @@
 // values per level each) go through a shared-memory ring per tile. Short
 // tiles (m <= 32) load the whole edge at once with cp.async and stage their
 // exports for one coalesced write-back; longer tiles stream the ring
-// (cp.async, kLook levels ahead). Inserts reload the two entering distances
+// (cp.async, kRing-2 levels ahead). Inserts reload the two entering distances
 // per side, exports store the two leaving ones.
 //
 // The instrumented debug kernel (heat_tile_debug_kernel) keeps an
