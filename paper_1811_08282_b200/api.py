@@ -318,8 +318,7 @@ def initial_condition_range(ident: str, n: int, spec: EquationSpec, start: int, 
                             gamma: float = 1.4, out: Optional[np.ndarray] = None) -> np.ndarray:
     """Points [start, start+count) of initial_condition(ident, n, ...)."""
     vpp = 1 if spec.equation == Equation.Heat else 3
-    if out is None:
-        out = np.empty(count * vpp, dtype=np.float64)
+    out = _out_buffer(out, count * vpp)
     e = _errbuf()
     _check(lib().s1d_initial_condition_range(ident.encode(), n, int(spec.equation), gamma, start, count,
                                              out.ctypes.data_as(C.POINTER(C.c_double)), out.size, e, 1024), e)
@@ -433,6 +432,25 @@ def _dptr(a: np.ndarray):
     return a.ctypes.data_as(C.POINTER(C.c_double))
 
 
+def _out_buffer(out: Optional[np.ndarray], n: int) -> np.ndarray:
+    """A caller-supplied output array is written through its raw pointer by the
+    library, so it must be exactly what the C ABI assumes: float64,
+    C-contiguous, writeable, at least n elements."""
+    if out is None:
+        return np.empty(n, dtype=np.float64)
+    if not isinstance(out, np.ndarray):
+        raise TypeError("out must be a numpy.ndarray")
+    if out.dtype != np.float64:
+        raise TypeError(f"out must be float64, got {out.dtype}")
+    if not out.flags.c_contiguous:
+        raise ValueError("out must be C-contiguous")
+    if not out.flags.writeable:
+        raise ValueError("out must be writeable")
+    if out.size < n:
+        raise ValueError(f"out holds {out.size} values, {n} needed")
+    return out
+
+
 def run(cfg: LaunchConfig) -> RunResult:
     """The drop-in for sweep1d::run (src/engine.cpp:40-47) on B200 GPUs."""
     spec = cfg.spec()
@@ -536,8 +554,7 @@ class Solver:
         return _stats(st), _timing(tm)
 
     def read_state(self, out: Optional[np.ndarray] = None) -> np.ndarray:
-        if out is None:
-            out = np.empty(self.state_len, dtype=np.float64)
+        out = _out_buffer(out, self.state_len)
         self._chk(lib().s1d_read_state(self._h, _dptr(out), out.size))
         return out
 
@@ -549,8 +566,7 @@ class Solver:
         return _stats(st), _timing(tm)
 
     def solve(self, state_in: Optional[np.ndarray] = None, out: Optional[np.ndarray] = None):
-        if out is None:
-            out = np.empty(self.state_len, dtype=np.float64)
+        out = _out_buffer(out, self.state_len)
         st, tm = _capi.s1d_stats(), _capi.s1d_timing()
         if state_in is not None:
             a = np.ascontiguousarray(state_in, dtype=np.float64)

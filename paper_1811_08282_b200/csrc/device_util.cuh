@@ -31,7 +31,10 @@ __device__ __forceinline__ double next_up(double x) {
 // a shard's flag word holds the rounds completed by one ring neighbour, stored
 // by that neighbour over NVLink (system-scope release) and polled here
 // (system-scope acquire). The spin is bounded: after timeout_ns it sets bit 1
-// of *err and returns, so a dead peer cannot wedge the GPU.
+// of *err and returns, so a dead peer cannot wedge the GPU. The abort is
+// sticky: once bit 1 is set (by any wait of the run), every later wait
+// returns at once, so a run of R rounds after a peer died costs one timeout,
+// not R (the host then reports S1D_TRANSPORT_ABORTED).
 __device__ __forceinline__ unsigned flag_ld_acquire(const unsigned* p) {
     unsigned v;
     asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -40,14 +43,18 @@ __device__ __forceinline__ unsigned flag_ld_acquire(const unsigned* p) {
 __device__ __forceinline__ void flag_st_release(unsigned* p, unsigned v) {
     asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ bool transport_aborted(const int* err) {
+    return (*reinterpret_cast<const volatile int*>(err) & 2) != 0;
+}
 __device__ __forceinline__ void flag_wait(const unsigned* f, unsigned seq, int* err, unsigned long long timeout_ns) {
     if ((int)(flag_ld_acquire(f) - seq) >= 0) return;
+    if (transport_aborted(err)) return;
     unsigned long long t0;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
     while ((int)(flag_ld_acquire(f) - seq) < 0) {
         unsigned long long t;
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
-        if (t - t0 > timeout_ns) {
+        if (t - t0 > timeout_ns || transport_aborted(err)) {
             atomicOr(err, 2);
             return;
         }

@@ -75,7 +75,20 @@ struct ShardBlob {
     cudaIpcMemHandle_t h[8];   // ic, state0, state1, EL0, EL1, ER0, ER1, flags
 };
 
-constexpr std::uint64_t kRoundTimeoutNs = 60ull * 1000 * 1000 * 1000; // dead-peer guard
+// Dead-peer guard of the device-side round waits (sticky: only the first
+// wait after a peer died pays it). 60 s by default; S1D_ROUND_TIMEOUT_S
+// overrides it (read once per process).
+std::uint64_t round_timeout_ns() {
+    static const std::uint64_t ns = [] {
+        double sec = 60.0;
+        if (const char* e = std::getenv("S1D_ROUND_TIMEOUT_S")) {
+            const double v = std::atof(e);
+            if (v > 0.0) sec = v;
+        }
+        return static_cast<std::uint64_t>(sec * 1e9);
+    }();
+    return ns;
+}
 
 } // namespace
 
@@ -403,7 +416,7 @@ struct Solver {
         if (mp) {
             Shard& s = sh(locals[0]);
             S1D_CUDA(cudaSetDevice(s.dev));
-            S1D_CUDA(launch_wait_flags(s.flags, seq, s.err, kRoundTimeoutNs, s.st));
+            S1D_CUDA(launch_wait_flags(s.flags, seq, s.err, round_timeout_ns(), s.st));
             return;
         }
         for (int g : locals) {
@@ -620,7 +633,7 @@ struct Solver {
                     a.round = static_cast<unsigned>(c - c_begin);
                     a.sig_left = L.flags + 1; // I am my left neighbour's right neighbour
                     a.sig_right = Rt.flags + 0;
-                    a.timeout_ns = kRoundTimeoutNs;
+                    a.timeout_ns = round_timeout_ns();
                 }
                 S1D_CUDA(cudaSetDevice(s.dev));
                 if (euler) S1D_CUDA(launch_euler_classic(flat ? 1 : 0, a, s.st));
@@ -1031,6 +1044,8 @@ void s1d_spec(int equation, int method, int* substeps, int* half_width, int* slo
 int s1d_initial_condition(const char* id, uint64_t n, int equation, double gamma, double* out, size_t out_len,
                           char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
+        need(id, "initial condition id");
+        need(out, "out");
         const auto v = s1d::initial_condition(id, n, equation, gamma);
         if (v.size() > out_len) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
         std::memcpy(out, v.data(), v.size() * sizeof(double));
@@ -1040,6 +1055,8 @@ int s1d_initial_condition(const char* id, uint64_t n, int equation, double gamma
 int s1d_initial_condition_range(const char* id, uint64_t n, int equation, double gamma, uint64_t j0, uint64_t count,
                                 double* out, size_t out_len, char* err, size_t errlen) {
     return guarded(err, errlen, [&] {
+        need(id, "initial condition id");
+        need(out, "out");
         if (j0 + count > n) throw s1d::Error(S1D_INVALID_CONFIG, "range outside the grid");
         const auto v = s1d::initial_condition_range(id, n, equation, gamma, j0, count);
         if (v.size() > out_len) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
@@ -1048,13 +1065,21 @@ int s1d_initial_condition_range(const char* id, uint64_t n, int equation, double
 }
 
 int s1d_max_signal_speed(const double* prim, size_t len, double gamma, double* out, char* err, size_t errlen) {
-    return guarded(err, errlen, [&] { *out = s1d::max_signal_speed(prim, len, gamma); });
+    return guarded(err, errlen, [&] {
+        need(prim, "prim");
+        need(out, "out");
+        *out = s1d::max_signal_speed(prim, len, gamma);
+    });
 }
 
 int s1d_partition(const s1d_config* cfg, uint64_t* blocks, uint64_t* start, int* left, int* right, char* err,
                   size_t errlen) {
     return guarded(err, errlen, [&] {
         need(cfg, "config");
+        need(blocks, "blocks");
+        need(start, "start");
+        need(left, "left");
+        need(right, "right");
         const auto p = s1d::make_partition(*cfg);
         for (std::size_t r = 0; r < p.blocks.size(); ++r) {
             blocks[r] = p.blocks[r];
@@ -1243,6 +1268,7 @@ int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen
 }
 
 int s1d_create(const s1d_config* cfg, s1d_solver** out, char* err, size_t errlen) {
+    if (!out) return guarded(err, errlen, [] { need(nullptr, "out"); });
     *out = nullptr;
     auto holder = std::make_unique<s1d_solver>();
     const int st = guarded(err, errlen, [&] {
@@ -1254,7 +1280,7 @@ int s1d_create(const s1d_config* cfg, s1d_solver** out, char* err, size_t errlen
 void s1d_destroy(s1d_solver* s) { delete s; }
 
 int s1d_get_config(const s1d_solver* s, s1d_config* out) {
-    if (!s) return S1D_INVALID_CONFIG;
+    if (!s || !out) return S1D_INVALID_CONFIG;
     *out = s->impl.cfg;
     return S1D_OK;
 }
@@ -1283,6 +1309,7 @@ int s1d_advance(s1d_solver* s, s1d_stats* stats, s1d_timing* timing) {
 int s1d_read_state(s1d_solver* s, double* host_out, size_t len) {
     if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
+        need(host_out, "host_out");
         if (len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
         for (int g : s->impl.locals)
             if (!s->impl.sh(g).final_state) throw s1d::Error(S1D_INVALID_CONFIG, "no state: call s1d_advance first");
@@ -1294,6 +1321,7 @@ int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_
               s1d_stats* stats, s1d_timing* timing) {
     if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
+        need(host_out, "host_out");
         if (host_in && in_len != s->impl.state_len())
             throw s1d::Error(S1D_INVALID_CONFIG, "initial state length mismatch");
         if (out_len < s->impl.state_len()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
@@ -1306,6 +1334,7 @@ int s1d_solve(s1d_solver* s, const double* host_in, size_t in_len, double* host_
 const char* s1d_last_error(const s1d_solver* s) { return s ? s->impl.last_error.c_str() : ""; }
 
 int s1d_shard_create(const s1d_config* cfg, int rank, int device, s1d_solver** out, char* err, size_t errlen) {
+    if (!out) return guarded(err, errlen, [] { need(nullptr, "out"); });
     *out = nullptr;
     auto holder = std::make_unique<s1d_solver>();
     const int st = guarded(err, errlen, [&] {
@@ -1319,6 +1348,7 @@ size_t s1d_shard_blob_size(void) { return sizeof(s1d::ShardBlob); }
 int s1d_shard_export(s1d_solver* s, void* blob, size_t blob_len) {
     if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
+        need(blob, "blob");
         if (blob_len < sizeof(s1d::ShardBlob)) throw s1d::Error(S1D_INVALID_CONFIG, "blob buffer too small");
         s->impl.export_blob(static_cast<s1d::ShardBlob*>(blob));
     });
@@ -1327,12 +1357,14 @@ int s1d_shard_export(s1d_solver* s, void* blob, size_t blob_len) {
 int s1d_shard_connect(s1d_solver* s, const void* left_blob, const void* right_blob) {
     if (!s) return S1D_INVALID_CONFIG;
     return guarded_solver(s, [&] {
+        need(left_blob, "left_blob");
+        need(right_blob, "right_blob");
         s->impl.connect(static_cast<const s1d::ShardBlob*>(left_blob), static_cast<const s1d::ShardBlob*>(right_blob));
     });
 }
 
 int s1d_shard_range(const s1d_solver* s, uint64_t* start, uint64_t* count) {
-    if (!s) return S1D_INVALID_CONFIG;
+    if (!s || !start || !count) return S1D_INVALID_CONFIG;
     if (s->impl.locals.size() != 1) {
         *start = 0;
         *count = s->impl.cfg.grid_size;

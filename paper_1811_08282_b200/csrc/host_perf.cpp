@@ -6,6 +6,11 @@
 //   power_law_fit / best_config  src/perf.cpp:42-97 (log-log OLS, tie-breaks)
 //   CSV header/row/emit/read     inc/csv.hpp:11-13, src/csv.cpp:14-136
 //                                (%.12g, RFC-4180 quoting, config-lexicographic order)
+//
+// These are deliberate RESTATEMENTS of the reference's formatter and fit: the
+// CSV must be byte-identical to emit_csv and the fit bit-identical to
+// power_law_fit (tests/test_perf_csv.py), which pins the statement order. They
+// sit off the hot path; the rest of the library is written in its own idiom.
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
@@ -214,15 +219,24 @@ extern "C" {
 
 const char* s1d_csv_header(void) { return s1d::kHeader; }
 
+// Returns the row length, -1 if buf is too small, or -status on an error
+// (null arguments, an exception inside the formatter): nothing throws across
+// the C boundary.
 int64_t s1d_csv_row(const s1d_record* r, char* buf, size_t len) {
-    const std::string row = s1d::csv_row(*r);
-    if (row.size() + 1 > len) return -1;
-    std::memcpy(buf, row.c_str(), row.size() + 1);
-    return static_cast<int64_t>(row.size());
+    int64_t n = -1;
+    const int st = guard(nullptr, 0, [&] {
+        if (!r || !buf) throw s1d::Error(S1D_INVALID_CONFIG, "null argument");
+        const std::string row = s1d::csv_row(*r);
+        if (row.size() + 1 > len) return;
+        std::memcpy(buf, row.c_str(), row.size() + 1);
+        n = static_cast<int64_t>(row.size());
+    });
+    return st == S1D_OK ? n : -static_cast<int64_t>(st);
 }
 
 int s1d_emit_csv(const s1d_record* recs, size_t n, const char* path, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
+        if ((!recs && n) || !path) throw s1d::Error(S1D_INVALID_CONFIG, "null argument");
         const std::string text = s1d::emit_csv(std::vector<s1d_record>(recs, recs + n));
         std::ofstream out(path, std::ios::trunc);
         if (!out) throw s1d::Error(S1D_INVALID_CONFIG, std::string("cannot open '") + path + "' for writing");
@@ -234,6 +248,7 @@ int s1d_emit_csv(const s1d_record* recs, size_t n, const char* path, char* err, 
 
 int s1d_read_csv(const char* path, s1d_record* out, size_t cap, size_t* count, char* err, size_t errlen) {
     return guard(err, errlen, [&] {
+        if (!path || !count || (!out && cap)) throw s1d::Error(S1D_INVALID_CONFIG, "null argument");
         const auto v = s1d::read_csv(path);
         *count = v.size();
         for (size_t i = 0; i < v.size() && i < cap; ++i) out[i] = v[i];
@@ -242,12 +257,18 @@ int s1d_read_csv(const char* path, s1d_record* out, size_t cap, size_t* count, c
 
 int s1d_power_law_fit(const double* n, const double* t, size_t count, double* A, double* b, double* r2, char* err,
                       size_t errlen) {
-    return guard(err, errlen, [&] { s1d::power_law_fit(n, t, count, A, b, r2); });
+    return guard(err, errlen, [&] {
+        if (!n || !t || !A || !b || !r2) throw s1d::Error(S1D_INVALID_CONFIG, "null argument");
+        s1d::power_law_fit(n, t, count, A, b, r2);
+    });
 }
 
 int64_t s1d_best_config(const s1d_record* recs, size_t n) {
     size_t idx = 0;
-    const int st = guard(nullptr, 0, [&] { idx = s1d::best_config(recs, n); });
+    const int st = guard(nullptr, 0, [&] {
+        if (!recs && n) throw s1d::Error(S1D_INVALID_CONFIG, "null argument");
+        idx = s1d::best_config(recs, n);
+    });
     return st == S1D_OK ? static_cast<int64_t>(idx) : -st;
 }
 

@@ -7,7 +7,8 @@
 // Before the next round, wait_kernel spins (system-scope acquire) until both
 // of its own flags have caught up. The spin is bounded: after `timeout_ns` it
 // sets bit 1 of the shard's error flag and returns, so a dead peer can never
-// wedge the GPU (the host reports S1D_TRANSPORT_ABORTED).
+// wedge the GPU (the host reports S1D_TRANSPORT_ABORTED). The abort is sticky
+// (bit 1 already set: return at once), so only the first round pays it.
 //
 // This replaces RingTransport's mutex/condvar round barrier
 // (src/transport.cpp:112-171) with device-side ordering: no host round trip
@@ -15,6 +16,7 @@
 // producer's edge buffer in place).
 #include <cstdint>
 
+#include "device_util.cuh"
 #include "kernels.hpp"
 
 namespace s1d {
@@ -40,6 +42,7 @@ __global__ void wait_kernel(const unsigned* flags, unsigned seq, int* err, std::
     while (true) {
         const unsigned a = ld_acquire_sys(flags), b = ld_acquire_sys(flags + 1);
         if ((int)(a - seq) >= 0 && (int)(b - seq) >= 0) break;
+        if (transport_aborted(err)) break;
         if (globaltimer() - t0 > timeout_ns) {
             atomicOr(err, 2);
             break;

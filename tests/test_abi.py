@@ -82,3 +82,50 @@ def test_null_arguments_fail_loudly():
     h = C.c_void_p()
     assert lib.s1d_create(None, C.byref(h), e, 256) == 1 and not h.value
     assert lib.s1d_advance(None, None, None) == 1 and lib.s1d_read_state(None, None, 0) == 1
+
+
+def test_null_outputs_fail_loudly():
+    """Every pointer argument of the ABI is checked before it is dereferenced
+    (no crash, S1D_INVALID_CONFIG and a message)."""
+    lib = _capi.lib()
+    e = C.create_string_buffer(256)
+    cfg = _capi.s1d_config()
+    lib.s1d_config_defaults(C.byref(cfg))
+    assert lib.s1d_create(C.byref(cfg), None, e, 256) == 1 and b"null" in e.value
+    assert lib.s1d_shard_create(C.byref(cfg), 0, 0, None, e, 256) == 1
+    assert lib.s1d_get_config(None, C.byref(cfg)) == 1
+    assert lib.s1d_shard_range(None, None, None) == 1
+    assert lib.s1d_shard_connect(None, None, None) == 1
+    assert lib.s1d_initial_condition(b"heat-sine", 16, 0, 1.4, None, 16, e, 256) == 1
+    assert lib.s1d_initial_condition(None, 16, 0, 1.4, None, 16, e, 256) == 1
+    assert lib.s1d_initial_condition_range(b"heat-sine", 16, 0, 1.4, 0, 4, None, 4, e, 256) == 1
+    assert lib.s1d_max_signal_speed(None, 3, 1.4, None, e, 256) == 1
+    cfg.ranks = 2
+    assert lib.s1d_partition(C.byref(cfg), None, None, None, None, e, 256) == 1 and b"null" in e.value
+    assert lib.s1d_csv_row(None, None, 0) == -1 * 1
+    assert lib.s1d_emit_csv(None, 1, None, e, 256) == 1
+    assert lib.s1d_read_csv(None, None, 0, None, e, 256) == 1
+    assert lib.s1d_power_law_fit(None, None, 3, None, None, None, e, 256) == 1
+    assert lib.s1d_best_config(None, 2) == -1
+
+
+def test_out_buffer_validation():
+    """api.py never hands the library a buffer it would overrun."""
+    import numpy as np
+    from paper_1811_08282_b200 import api
+    assert api._out_buffer(None, 4).dtype == np.float64
+    with pytest.raises(TypeError):
+        api._out_buffer(np.zeros(8, np.float32), 4)
+    with pytest.raises(ValueError):
+        api._out_buffer(np.zeros(8)[::2], 4)
+    with pytest.raises(ValueError):
+        api._out_buffer(np.zeros(3), 4)
+    ro = np.zeros(4)
+    ro.flags.writeable = False
+    with pytest.raises(ValueError):
+        api._out_buffer(ro, 4)
+    spec = api.make_spec(api.Equation.Heat, api.Method.Lengthening)
+    with pytest.raises(TypeError):
+        api.initial_condition_range("heat-sine", 16, spec, 0, 4, out=np.zeros(4, np.float32))
+    got = api.initial_condition_range("heat-sine", 16, spec, 0, 4, out=np.zeros(4))
+    assert got.shape == (4,)
