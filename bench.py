@@ -134,10 +134,73 @@ def dist_init():
     return rank, world
 
 
+def relaunch_under_torchrun(argv, n):
+    """`python bench.py --gpus N` outside a launcher: re-exec this script under
+    torch.distributed.run with N processes (one per GPU), the same launch the
+    driver uses; the JSON line comes from rank 0 of that job."""
+    import socket
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+    sys.stdout.flush()
+    sys.stderr.flush()
+    os.execv(sys.executable, cmd)
+
+
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def barrier(world):
     if world > 1:
         import torch.distributed as dist
         dist.barrier()
+
+
+def ring_connect_record(rank, world, local, shard):
+    """After the shards are connected: one line per rank on stderr with the
+    ring it joined (the data plane is peer-pointer reads over NVLink, not a
+    NCCL collective), and - when every rank has its own GPU - a NCCL
+    communicator over the same ranks, checked with one all-reduce, so the job's
+    GPU set is visible to NCCL_DEBUG as well. Returns rank 0's summary."""
+    import torch
+    import torch.distributed as dist
+    start, count = shard.start, shard.count
+    left, right = (rank + world - 1) % world, (rank + 1) % world
+    nccl_ok = None
+    if torch.cuda.is_available() and world <= torch.cuda.device_count():
+        try:
+            torch.cuda.set_device(local)
+            g = dist.new_group(backend="nccl")
+            t = torch.ones(1, device=f"cuda:{local}")
+            dist.all_reduce(t, group=g)
+            torch.cuda.synchronize(local)
+            nccl_ok = int(t.item()) == world
+        except Exception as ex:  # reported, the data plane does not depend on it
+            nccl_ok = f"nccl group unavailable: {ex!r}"[:200]
+    print(f"[bench] ring connect: rank {rank} nranks {world} cudaDev {local} left {left} right {right} "
+          f"shard [{start}, {start + count}) nccl_allreduce_ok {nccl_ok}", file=sys.stderr, flush=True)
+    recs = [None] * world
+    dist.all_gather_object(recs, {"rank": rank, "device": local, "start": start, "count": count})
+    return {"nranks": world, "devices": [r["device"] for r in recs],
+            "shards": [[r["start"], r["count"]] for r in recs], "nccl_allreduce_ok": nccl_ok,
+            "transport": "peer-pointer edge reads over NVLink (CUDA IPC) + device flags, one message per "
+                         "shard per half-cycle"}
 
 
 def allmax(world, x: float) -> float:
@@ -161,6 +224,10 @@ def divisor_ranks(blocks: int, want: int) -> int:
 
 
 def cpu_reference_sample(equation, scheme, w, n_sample, steps, threads):
+    """One run of the reference's own engine (sweep1d::run, compiled from
+    source into oracle/_ref) with one rank thread per host core (the reference
+    runs R rank threads, engines_impl.hpp:35-67; R must divide the block count
+    and be >= 2, config.cpp:79-81)."""
     from oracle import oracle as O
     blocks = n_sample // w
     ranks = max(divisor_ranks(blocks, threads), 2)
@@ -171,33 +238,55 @@ def cpu_reference_sample(equation, scheme, w, n_sample, steps, threads):
     return rate, ranks, res.loop_seconds
 
 
+def reference_sample_size(args, timed_steps):
+    """The reference arm's per-step sample: the B200 arm's grid (n = 2^log2n,
+    same w) for T = m = w/2 time steps (one swept cycle: Up + Down, no classic
+    pad; T < m would be all pad, swept_worker :313-320). Only T differs from
+    the GPU arm. If `timed_steps` of it would overrun --ref-budget-s (measured
+    rate from a small calibration run), n is halved until it fits, and the
+    line says so."""
+    m = args.w // 2
+    steps = args.ref_steps or m
+    steps = max(m, (steps // m) * m)
+    n = args.ref_n or (1 << args.log2n)
+    rate, _, _ = cpu_reference_sample(args.equation, args.scheme, args.w, min(n, 1 << 22), m, host_cores())
+    while n > args.w * 64 and timed_steps * n * steps / rate > args.ref_budget_s:
+        n //= 2
+    return n, steps, rate
+
+
 def run_reference_arm(args, rank, world):
     if rank != 0:
-        return 0
-    threads = os.cpu_count() or 1
+        return 0  # the CPU reference runs once, on rank 0 (the host's cores are shared)
+    threads = host_cores()
     w = args.w
-    m = w // 2
-    n_sample = args.ref_n
-    steps_sample = max(m, (args.ref_steps // m) * m)
-    vals = []
     t_all = time.perf_counter()
+    n_sample, steps_sample, _ = reference_sample_size(args, args.steps)
+    vals, ranks = [], 0
     for i in range(args.warmup + args.steps):
-        rate, ranks, secs = cpu_reference_sample(args.equation, args.scheme, w, n_sample, steps_sample, threads)
+        # warm-up steps run a small sample (untimed); timed steps the full one
+        n_i = n_sample if i >= args.warmup else min(n_sample, 1 << 22)
+        rate, ranks, secs = cpu_reference_sample(args.equation, args.scheme, w, n_i, steps_sample, threads)
         if i >= args.warmup:
             vals.append(rate)
     value = statistics.mean(vals) / 1e6
-    sample = (f"sweep1d::run({args.scheme}, WallClock) heat n=2^{n_sample.bit_length() - 1} w={w} "
-              f"T={steps_sample} per step ({ranks} rank threads); throughput per point is size-independent "
-              f"past cache, so the sample stands for the n=2^{args.log2n} workload")
+    same_n = n_sample == (1 << args.log2n)
+    sample = (f"sweep1d::run({args.scheme}, WallClock) {args.equation} n=2^{n_sample.bit_length() - 1} w={w} "
+              f"T={steps_sample} per step, {ranks} rank threads on {threads} host cores"
+              + ("; only T differs from the GPU arm (T = m: one swept cycle, no pad)" if same_n else
+                 f"; n reduced from 2^{args.log2n} to fit --ref-budget-s {args.ref_budget_s:g}")
+              + (f"; rank 0 of {world}, per-point throughput (the host's cores do not grow with N)"
+                 if world > 1 else ""))
     line = {
         "metric": METRIC, "value": round(value, 3), "unit": UNIT, "impl": "reference", "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": round(1e3 * n_sample * steps_sample / (value * 1e6), 3), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (heat-sine IC)",
         "config": {"workload": workload_name(args), "equation": args.equation, "scheme": args.scheme,
-                   "grid_size": n_sample, "block_width": w, "steps_per_run": steps_sample},
+                   "grid_size": n_sample, "block_width": w, "steps_per_run": steps_sample,
+                   "same_config_except_T": same_n},
         "cpu_baseline": {"value": round(value, 3), "unit": UNIT, "cores": ranks, "kind": "reference",
-                         "sample": sample},
+                         "host_cores": threads, "cpu_model": cpu_model(), "sample": sample},
         "e2e": {"value": round(value, 3), "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
         "wall_seconds": round(time.perf_counter() - t_all, 2),
     }
@@ -231,10 +320,12 @@ def run_b200(args, rank, world):
         cfg = s1d.LaunchConfig(equation=eq, scheme=scheme, grid_size=n_total, block_width=args.w, ranks=world,
                                steps=args.T)
         solver = open_ring_shard(cfg, rank, world, local)
+        ring = ring_connect_record(rank, world, local, solver)
     else:
         cfg = s1d.LaunchConfig(equation=eq, scheme=scheme, grid_size=n_per, block_width=args.w, ranks=1,
                                steps=args.T, num_devices=1)
         solver = s1d.Solver(cfg)
+        ring = {"nranks": 1, "devices": [local], "transport": "single shard (periodic ring of one)"}
     # warm-up
     for _ in range(args.warmup):
         solver.advance()
@@ -343,13 +434,13 @@ def run_b200(args, rank, world):
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            threads = os.cpu_count() or 1
-            rate, ranks, secs = cpu_reference_sample(args.equation, args.scheme, args.w, args.ref_n,
-                                                     max(args.w // 2, (args.ref_steps // (args.w // 2)) * (args.w // 2)),
-                                                     threads)
+            threads = host_cores()
+            n_s, t_s, _ = reference_sample_size(args, 1)
+            rate, ranks, secs = cpu_reference_sample(args.equation, args.scheme, args.w, n_s, t_s, threads)
             cpu = {"value": round(rate / 1e6, 3), "unit": UNIT, "cores": ranks, "kind": "reference",
-                   "sample": f"sweep1d::run({args.scheme}, WallClock) n=2^{args.ref_n.bit_length() - 1} "
-                             f"w={args.w} T={args.ref_steps}, {ranks} rank threads, {secs:.1f} s"}
+                   "host_cores": threads, "cpu_model": cpu_model(),
+                   "sample": f"sweep1d::run({args.scheme}, WallClock) n=2^{n_s.bit_length() - 1} "
+                             f"w={args.w} T={t_s}, {ranks} rank threads, {secs:.1f} s"}
         except Exception as ex:
             cpu = {"value": None, "unit": UNIT, "error": repr(ex)}
 
@@ -365,7 +456,7 @@ def run_b200(args, rank, world):
                        "steps_per_run": args.T, "parallelism": f"shards{world}",
                        "l2": "inputs larger than L2 (1 GiB state per GPU vs 126 MB L2)"},
             "us_per_timestep": round(1e6 * loop_s / args.steps / args.T, 3),
-            "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+            "clocks": clocks, "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "ring": ring,
             "classic_same_grid": classic, "euler_sod": euler, "cpu_baseline": cpu,
             "wall_seconds_timed_region": round(wall, 3),
         }
@@ -404,12 +495,18 @@ def main(argv=None):
     ap.add_argument("--euler-log2n", type=int, default=22)
     ap.add_argument("--euler-w", type=int, default=512)
     ap.add_argument("--euler-T", type=int, default=1024)
-    ap.add_argument("--ref-n", type=int, default=1 << 25, help="CPU reference sample grid size")
-    ap.add_argument("--ref-steps", type=int, default=2048, help="CPU reference sample time steps")
+    ap.add_argument("--ref-n", type=int, default=0, help="CPU reference sample grid size (default: 2^log2n)")
+    ap.add_argument("--ref-steps", type=int, default=0, help="CPU reference sample time steps (default: w/2)")
+    ap.add_argument("--ref-budget-s", type=float, default=420.0,
+                    help="upper bound on the reference arm's timed CPU work (n is halved to fit)")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3  # timing rule: >= 3 warm-up steps
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        relaunch_under_torchrun(sys.argv[1:] if argv is None else argv, args.gpus)
     rank, world = dist_init()
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but the launcher started {world} processes")
     if args.impl == "reference":
         return run_reference_arm(args, rank, world)
     return run_b200(args, rank, world)
