@@ -164,6 +164,43 @@ inline RunResult run(const LaunchConfig& cfg) {
     return r;
 }
 
+/// Run instrumentation hooks (the subset of sweep1d::RunOptions,
+/// inc/debug.hpp:17-24, that the B200 path implements). Any hook set routes the
+/// run through the instrumented kernels (s1d_run_debug: same geometry and
+/// arithmetic, slower).
+struct RunOptions {
+    bool coverage = false;    // count every (point, substep) computation
+    bool perturb_ulp = false; // nudge the first kernel write by 1 ulp (mutation hook)
+};
+
+/// sweep1d::run(cfg, opts) (inc/engine.hpp:28). With coverage on, `coverage`
+/// receives [steps*S][n] counts (index (substep-1)*n + point) when non-null.
+inline RunResult run(const LaunchConfig& cfg, const RunOptions& opts, std::vector<std::uint32_t>* coverage = nullptr) {
+    if (!opts.coverage && !opts.perturb_ulp) return run(cfg);
+    const s1d_config c = cfg.to_c();
+    RunResult r;
+    r.state.resize(cfg.grid_size * static_cast<std::size_t>(cfg.values_per_point()));
+    std::vector<std::uint32_t> cov;
+    s1d_debug d{};
+    d.coverage = opts.coverage ? 1 : 0;
+    d.perturb_ulp = opts.perturb_ulp ? 1 : 0;
+    if (opts.coverage) {
+        int S = 1;
+        s1d_spec(c.equation, c.method, &S, nullptr, nullptr, nullptr);
+        cov.assign(static_cast<std::size_t>(cfg.steps) * static_cast<std::size_t>(S) * cfg.grid_size, 0u);
+        d.coverage_out = cov.data();
+        d.coverage_len = cov.size();
+    }
+    s1d_stats st;
+    s1d_timing tm;
+    char err[512];
+    check(s1d_run_debug(&c, &d, r.state.data(), r.state.size(), &st, &tm, err, sizeof err), err);
+    r.stats = CommStats{st.messages_sent, st.bytes_sent, st.exchange_rounds, st.kernel_launches};
+    r.timing = EngineTiming{tm.setup_seconds, tm.loop_seconds, tm.virtual_seconds};
+    if (coverage) *coverage = std::move(cov);
+    return r;
+}
+
 using TimingRecord = s1d_record;
 
 inline TimingRecord measure(const LaunchConfig& cfg) {

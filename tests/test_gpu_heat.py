@@ -29,7 +29,8 @@ def assert_bitwise(got, want):
 
 
 @pytest.mark.parametrize("scheme", [s1d.Scheme.Swept, s1d.Scheme.Classic])
-@pytest.mark.parametrize("steps,fnv", [(64, "4185347ae18fab0f"), (1000, "90d783358019c683")])
+@pytest.mark.parametrize("steps,fnv", [(64, "4185347ae18fab0f"), (1000, "90d783358019c683"),
+                                       (6144, "389326b8952bc813")])
 def test_fingerprint_n16k_w64(gpu, scheme, steps, fnv):
     res = s1d.run(cfg(scheme, 1 << 14, 64, steps))
     assert O.fnv1a64(res.state) == fnv

@@ -3,7 +3,8 @@
 // "bench-cli" describes) on the C++ host interface include/swept1d.hpp.
 //
 //   s1d solve  [--config F] [key=value ...] [--dump F]  one run: CSV row + fingerprint
-//   s1d verify [--config F] [key=value ...]             swept vs classic, bitwise
+//   s1d verify [--config F] [--against DUMP] [--perturb-ulp] [key=value ...]
+//                                                       swept vs classic vs serial oracle, bitwise
 //   s1d sweep  --n N1,N2.. --w W1,W2.. [--wf A,B..] [--schemes swept,classic]
 //              [key=value ...] --out F.csv              measure a grid, emit CSV
 //   s1d fit    F.csv [--scheme swept|classic]            Table-1 power law over best configs
@@ -13,6 +14,7 @@
 // equation, method, scheme, n|grid_size, w|block_width, ranks, wf|work_factor,
 // steps, initial, mode, fourier, gamma, cfl, alpha, beta, compute_cost
 // (+ num_devices). Precedence: key=value arguments > --config file > defaults.
+#include <cmath>
 #include <cstdint>
 #include <cstdio>
 #include <cstdlib>
@@ -136,29 +138,70 @@ int cmd_solve(const Args& a) {
     return 0;
 }
 
+// Bitwise comparison of two states: mismatch count and max |diff|, where a
+// mismatch involving a NaN counts as an infinite difference.
+struct Diff {
+    std::size_t mismatches = 0;
+    double max_abs = 0.0;
+};
+
+Diff compare(const std::vector<double>& a, const std::vector<double>& b) {
+    Diff d;
+    for (std::size_t i = 0; i < a.size(); ++i) {
+        if (std::memcmp(&a[i], &b[i], sizeof(double)) == 0) continue;
+        ++d.mismatches;
+        const double x = std::isnan(a[i]) || std::isnan(b[i]) ? INFINITY : std::fabs(a[i] - b[i]);
+        if (x > d.max_abs) d.max_abs = x;
+    }
+    return d;
+}
+
+bool report_pair(const char* what, const Diff& d, std::size_t n) {
+    std::printf("%s: bitwise: %s, max|diff| = %.17g (%zu of %zu values differ)\n", what,
+                d.mismatches == 0 ? "true" : "false", d.max_abs, d.mismatches, n);
+    return d.mismatches == 0;
+}
+
+std::vector<double> read_dump(const std::string& path, std::size_t want) {
+    std::ifstream in(path, std::ios::binary | std::ios::ate);
+    if (!in) throw std::runtime_error("cannot open '" + path + "'");
+    const auto bytes = static_cast<std::size_t>(in.tellg());
+    if (bytes != want * sizeof(double))
+        throw InvalidConfig("'" + path + "' holds " + std::to_string(bytes) + " bytes, " +
+                            std::to_string(want * sizeof(double)) + " expected (n*vpp doubles)");
+    std::vector<double> v(want);
+    in.seekg(0);
+    in.read(reinterpret_cast<char*>(v.data()), static_cast<std::streamsize>(bytes));
+    if (!in) throw std::runtime_error("cannot read '" + path + "'");
+    return v;
+}
+
+// SPEC.md bench-cli verify: swept vs classic vs the serial oracle, max |diff|
+// and a bitwise flag per pair; non-zero exit on any difference, in
+// particular on an injected 1-ulp kernel perturbation (--perturb-ulp, the
+// reference's RunOptions::perturb_ulp, applied to the swept run). The serial
+// leg is a dump of the reference's run_serial (--against FILE, written by
+// oracle/dump_serial.py): the oracle is test infrastructure and is never
+// linked into the product.
 int cmd_verify(const Args& a) {
     LaunchConfig sw = a.cfg, cl = a.cfg;
     sw.scheme = Scheme::Swept;
     cl.scheme = Scheme::Classic;
-    const RunResult rs = run(sw), rc = run(cl);
-    double maxdiff = 0.0;
-    std::size_t mism = 0;
-    for (std::size_t i = 0; i < rs.state.size(); ++i) {
-        if (std::memcmp(&rs.state[i], &rc.state[i], sizeof(double)) != 0) ++mism;
-        const double d = rs.state[i] > rc.state[i] ? rs.state[i] - rc.state[i] : rc.state[i] - rs.state[i];
-        if (d > maxdiff) maxdiff = d;
-    }
-    bool ok = mism == 0;
-    std::printf("swept vs classic: bitwise: %s, max|diff| = %.17g (%zu of %zu values differ)\n", ok ? "true" : "false",
-                maxdiff, mism, rs.state.size());
+    RunOptions opts;
+    opts.perturb_ulp = a.flags.count("perturb-ulp") != 0;
+    const RunResult rs = run(sw, opts), rc = run(cl);
+    const std::size_t n = rs.state.size();
+    if (opts.perturb_ulp) std::printf("swept run perturbed by 1 ulp (mutation hook)\n");
+    bool ok = report_pair("swept vs classic", compare(rs.state, rc.state), n);
     if (a.flags.count("against")) {
-        std::ifstream in(a.flags.at("against"), std::ios::binary);
-        std::vector<double> ref(rs.state.size());
-        in.read(reinterpret_cast<char*>(ref.data()), static_cast<std::streamsize>(ref.size() * sizeof(double)));
-        const bool same = in && std::memcmp(ref.data(), rs.state.data(), ref.size() * sizeof(double)) == 0;
-        std::printf("swept vs %s: bitwise: %s\n", a.flags.at("against").c_str(), same ? "true" : "false");
-        ok = ok && same;
+        const auto ref = read_dump(a.flags.at("against"), n);
+        const std::string p = a.flags.at("against");
+        ok = report_pair(("swept vs serial oracle " + p).c_str(), compare(rs.state, ref), n) && ok;
+        ok = report_pair(("classic vs serial oracle " + p).c_str(), compare(rc.state, ref), n) && ok;
+    } else {
+        std::printf("serial oracle: not given (--against DUMP, from oracle/dump_serial.py)\n");
     }
+    std::printf("verify: %s\n", ok ? "PASS" : "FAIL");
     return ok ? 0 : 1;
 }
 
@@ -266,7 +309,7 @@ int usage() {
     std::fprintf(stderr,
                  "usage: s1d solve|verify|sweep|fit|report [options] [key=value ...]\n"
                  "  solve  [--config F] [--dump F] key=value...\n"
-                 "  verify [--config F] [--against F] key=value...\n"
+                 "  verify [--config F] [--against DUMP] [--perturb-ulp] key=value...\n"
                  "  sweep  --n 2^20,2^22 --w 64,1024 [--wf 0,2] [--schemes swept,classic] --out F.csv key=value...\n"
                  "  fit    F.csv [--scheme swept|classic]\n"
                  "  report F.csv\n"
