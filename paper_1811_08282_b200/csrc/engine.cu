@@ -44,6 +44,7 @@ struct CudaError : Error {
 struct Shard {
     bool local = true;        // false: a view of a neighbour shard owned by another process
     int dev = 0;
+    int sms = 148;            // SM count of dev (grid sizing; queried once)
     cudaStream_t st = nullptr;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr, ev_done = nullptr;
     cudaEvent_t ev_dom0 = nullptr, ev_dom1 = nullptr; // around the dominant kernel's launches
@@ -78,6 +79,21 @@ struct ShardBlob {
 // Dead-peer guard of the device-side round waits (sticky: only the first
 // wait after a peer died pays it). 60 s by default; S1D_ROUND_TIMEOUT_S
 // overrides it (read once per process).
+// SM count of a device (grid sizing), cached per device.
+int device_sms(int dev) {
+    static int cache[64] = {};
+    if (dev < 0 || dev >= 64) return 148;
+    if (cache[dev] <= 0) {
+        int v = 0;
+        if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) {
+            cudaGetLastError();
+            v = 148;
+        }
+        cache[dev] = v;
+    }
+    return cache[dev];
+}
+
 std::uint64_t round_timeout_ns() {
     static const std::uint64_t ns = [] {
         double sec = 60.0;
@@ -196,10 +212,7 @@ struct Solver {
                     throw Error(S1D_INVALID_WIDTH,
                                 "block width " + std::to_string(cfg.block_width) +
                                     " has no tile decomposition on the B200 path "
-                                    "(needs w/P <= 1024 threads for some P in {2,4,8,16} dividing w)");
-            } else if (euler_tile_smem_bytes(flat ? 1 : 0, static_cast<int>(cfg.block_width)) > 227 * 1024) {
-                throw Error(S1D_INVALID_WIDTH, "block width " + std::to_string(cfg.block_width) +
-                                                   " exceeds the shared-memory-resident Euler tile (227 KB per CTA)");
+                                    "(w/2 distances per side need at most 1024 slots of 8: w <= 16384)");
             }
         }
         int visible = 0;
@@ -269,6 +282,7 @@ struct Solver {
         configure(in);
         for (int g = 0; g < R(); ++g) {
             sh(g).dev = g % ndev;
+            sh(g).sms = device_sms(sh(g).dev);
             locals.push_back(g);
         }
         for (int g = 0; g < R(); ++g) {
@@ -296,6 +310,7 @@ struct Solver {
         Shard& me = sh(rank);
         me.local = true;
         me.dev = device;
+        me.sms = device_sms(device);
         locals.push_back(rank);
         allocate(me);
         connected = R() == 1;
@@ -626,6 +641,7 @@ struct Solver {
                 a.gamma = cfg.gamma;
                 a.dt_dx = cfg.dt_dx;
                 a.error_flag = s.err;
+                a.sms = s.sms;
                 a.dbg = dbg_args(g);
                 if (fused) {
                     a.nb_flags = s.flags;
@@ -681,6 +697,7 @@ struct Solver {
             a.gamma = cfg.gamma;
             a.dt_dx = cfg.dt_dx;
             a.error_flag = s.err;
+            a.sms = s.sms;
             a.dbg = dbg_args(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             auto launch = [&](const TileArgs& ta) {

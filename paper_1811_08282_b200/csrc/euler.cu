@@ -242,21 +242,30 @@ inline int euler_tiles_per_cta(int flat, int w) {
 
 // MAXT = 1024: one thread per point of the widest span (latency-bound small
 // grids, where the CTA count is below one wave).
-template <int FLAT, int KIND, bool DBG, int MAXT>
+// GMEM: tiles whose records exceed a CTA's shared memory (lengthening
+// w > ~2600, flattening w > ~2800; the reference's check_width has no upper
+// bound, R/core/src/swept.cpp:10-19) keep records, pressures and fluxes in a
+// per-CTA global scratch block (L1/L2-resident) and only the edge ring in
+// shared memory; same code, same barriers, same arithmetic.
+template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false>
 __global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1 : S1D_EULER_MINB) euler_tile(const TileArgs a, int GT) {
     using G = TileGeom<FLAT>;
     constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
     extern __shared__ double sm[];
     const int w = a.w, m = a.m, t = threadIdx.x, NT = blockDim.x;
     const int W2 = w + 2 * H;
-    const std::size_t TS = (std::size_t)REC * W2 + 4 * (std::size_t)(W2 + 1) + 2 * (std::size_t)kERing * LVL;
+    const std::size_t TR = (std::size_t)REC * W2 + 4 * (std::size_t)(W2 + 1); // records + pressures + fluxes
+    const std::size_t TRING = 2 * (std::size_t)kERing * LVL;
+    const std::size_t TS = TR + TRING;
     // per-tile views: S [REC][W2] records (local x in [0, W2)), P [W2+1]
     // pressures, Fx [3][W2+1] interface fluxes (interface x between x-1 and
     // x), ring [2 sides][kERing][LVL]
-    auto S = [&](int gi) { return sm + gi * TS; };
-    auto Pp = [&](int gi) { return sm + gi * TS + REC * W2; };
-    auto Fx = [&](int gi) { return sm + gi * TS + REC * W2 + (W2 + 1); };
-    auto ring = [&](int gi) { return sm + gi * TS + REC * W2 + 4 * (W2 + 1); };
+    double* const tbase = GMEM ? a.scratch + (std::size_t)blockIdx.x * GT * TR : sm;
+    const std::size_t tstep = GMEM ? TR : TS;
+    auto S = [&](int gi) { return tbase + gi * tstep; };
+    auto Pp = [&](int gi) { return tbase + gi * tstep + REC * W2; };
+    auto Fx = [&](int gi) { return tbase + gi * tstep + REC * W2 + (W2 + 1); };
+    auto ring = [&](int gi) { return GMEM ? sm + gi * TRING : sm + gi * TS + TR; };
     const double gamma = a.gamma;
     const double dt_dx = a.dt_dx;
     const std::size_t tstride = (std::size_t)w * REC; // edge doubles per tile per side
@@ -497,13 +506,29 @@ __global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1 : S1D_EULER_MINB) euler_t
     raise_flag(a.error_flag, bad);
 }
 
-template <int FLAT, bool DBG = false, int MAXT = 256>
-cudaError_t launch_tile_f(int kind, const TileArgs& a, cudaStream_t st, int cap_threads = 0) {
-    const int GT = euler_tiles_per_cta(FLAT, a.w);
-    const size_t smem = (size_t)GT * euler_tile_smem(FLAT, a.w);
-    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT>
-                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT>
-                                                        : euler_tile<FLAT, kDown, DBG, MAXT>;
+// Largest dynamic shared memory a CTA may opt into (read once per process).
+std::size_t smem_optin() {
+    static const std::size_t v = [] {
+        int dev = 0, b = 0;
+        cudaGetDevice(&dev);
+        if (cudaDeviceGetAttribute(&b, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess || b <= 0) {
+            cudaGetLastError();
+            b = 227 * 1024;
+        }
+        return (std::size_t)b;
+    }();
+    return v;
+}
+
+template <int FLAT, bool DBG = false, int MAXT = 256, bool GMEM = false>
+cudaError_t launch_tile_f(int kind, const TileArgs& a_in, cudaStream_t st, int cap_threads = 0) {
+    TileArgs a = a_in;
+    const int GT = GMEM ? 1 : euler_tiles_per_cta(FLAT, a.w);
+    const std::size_t ring_doubles = 2 * (std::size_t)kERing * TileGeom<FLAT>::LVL;
+    const size_t smem = GMEM ? GT * ring_doubles * sizeof(double) : (size_t)GT * euler_tile_smem(FLAT, a.w);
+    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, GMEM>
+                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, GMEM>
+                                                        : euler_tile<FLAT, kDown, DBG, MAXT, GMEM>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -519,8 +544,18 @@ cudaError_t launch_tile_f(int kind, const TileArgs& a, cudaStream_t st, int cap_
     const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
     if (count <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((count + GT - 1) / GT);
+    if (GMEM) { // stream-ordered scratch for this launch (graph-capturable)
+        const std::size_t bytes = sizeof(double) * grid * GT * (euler_tile_doubles(FLAT, a.w) - ring_doubles);
+        cudaError_t e = cudaMallocAsync(reinterpret_cast<void**>(&a.scratch), bytes, st);
+        if (e != cudaSuccess) return e;
+    }
     k<<<grid, nt, smem, st>>>(a, GT);
-    return cudaGetLastError();
+    cudaError_t e = cudaGetLastError();
+    if (GMEM) {
+        const cudaError_t f = cudaFreeAsync(a.scratch, st);
+        if (e == cudaSuccess) e = f;
+    }
+    return e;
 }
 
 __global__ void unpack_kernel(const double* __restrict__ aos, double* __restrict__ st, std::uint64_t N,
@@ -548,10 +583,7 @@ __global__ void pack_kernel(const double* __restrict__ st, double* __restrict__ 
     }
 }
 
-unsigned grid_for(std::uint64_t n, int per_block) {
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+unsigned grid_for(std::uint64_t n, int per_block, int sms) {
     std::uint64_t blocks = (n + per_block - 1) / per_block;
     const std::uint64_t cap = (std::uint64_t)sms * 16;
     if (blocks > cap) blocks = cap;
@@ -561,7 +593,7 @@ unsigned grid_for(std::uint64_t n, int per_block) {
 } // namespace
 
 cudaError_t launch_euler_classic(int flat, const ClassicArgs& a, cudaStream_t st) {
-    const unsigned grid = grid_for(a.N, kClassicB);
+    const unsigned grid = grid_for(a.N, kClassicB, a.sms);
     if (flat) {
         if (a.counter & 1) euler_flat_classic<0><<<grid, kClassicB, 0, st>>>(a);
         else euler_flat_classic<1><<<grid, kClassicB, 0, st>>>(a);
@@ -577,17 +609,17 @@ cudaError_t launch_euler_classic(int flat, const ClassicArgs& a, cudaStream_t st
 }
 
 cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_t st, bool debug) {
+    if (euler_tile_smem(flat, a.w) > smem_optin()) { // records in global scratch
+        if (debug) return flat ? launch_tile_f<1, true, 256, true>(kind, a, st)
+                               : launch_tile_f<0, true, 256, true>(kind, a, st);
+        return flat ? launch_tile_f<1, false, 1024, true>(kind, a, st, 512)
+                    : launch_tile_f<0, false, 1024, true>(kind, a, st, 512);
+    }
     if (debug) return flat ? launch_tile_f<1, true>(kind, a, st) : launch_tile_f<0, true>(kind, a, st);
     // Latency-bound launches (at most one CTA per SM, e.g. 2^16 points per GPU)
     // run one thread per span point (1024-thread CTAs): measured +15-20% at
     // 2^16; with more CTAs than SMs the 256-thread build's occupancy wins (2x).
-    static int sms = 0;
-    if (sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-        if (sms <= 0) sms = 148;
-    }
+    const int sms = a.sms;
     const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
     const int GT = euler_tiles_per_cta(flat, a.w);
     bool wide = (count + GT - 1) / GT <= sms;
@@ -602,13 +634,13 @@ cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_
 
 cudaError_t launch_euler_unpack(const double* aos, double* st_fields, std::uint64_t N, std::uint64_t fs, int rec,
                                 cudaStream_t st) {
-    unpack_kernel<<<grid_for(N, 256), 256, 0, st>>>(aos, st_fields, N, fs, rec);
+    unpack_kernel<<<grid_for(N, 256, 148), 256, 0, st>>>(aos, st_fields, N, fs, rec);
     return cudaGetLastError();
 }
 
 cudaError_t launch_euler_pack(const double* st_fields, double* aos, std::uint64_t N, std::uint64_t fs,
                               cudaStream_t st) {
-    pack_kernel<<<grid_for(N, 256), 256, 0, st>>>(st_fields, aos, N, fs);
+    pack_kernel<<<grid_for(N, 256, 148), 256, 0, st>>>(st_fields, aos, N, fs);
     return cudaGetLastError();
 }
 

@@ -40,7 +40,11 @@ namespace s1d {
 namespace {
 
 __device__ __forceinline__ double heat_f(double l, double c, double r, double fo) {
+#ifdef S1D_EXP_FMA
+    return __dadd_rn(c, __dmul_rn(fo, __dadd_rn(__fma_rn(-2.0, c, l), r)));
+#else
     return __dadd_rn(c, __dmul_rn(fo, __dadd_rn(__dsub_rn(l, __dmul_rn(2.0, c)), r)));
+#endif
 }
 
 __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) {
@@ -98,12 +102,8 @@ template <int N>
 __device__ __forceinline__ void cp_async_wait() { asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory"); }
 
 // Diagnostic builds (-DS1D_NO_LEVEL_BARRIER) replace the level barrier with
-// __syncwarp() to time the level loop without it (results are then wrong).
-#ifdef S1D_NO_LEVEL_BARRIER
-#define S1D_LEVEL_BARRIER() __syncwarp()
-#else
-#define S1D_LEVEL_BARRIER() __syncthreads()
-#endif
+// __syncwarp() to time the level loop without it (results are then wrong);
+// see level_sync.
 
 // ---------------------------------------------------------------------------
 // Production tile kernel: folded, slot-major layout.
@@ -166,6 +166,17 @@ struct Fold {
     const double* ringR; // left producer's R edges
     const double* ringL; // right producer's L edges
 };
+
+// One CTA barrier per level. (Neighbour-only synchronisation — hardware named
+// barriers per pair of neighbour warps — was measured 23% slower, DESIGN.md
+// section 8.) Diagnostic builds (-DS1D_NO_LEVEL_BARRIER) drop it.
+__device__ __forceinline__ void level_sync() {
+#ifdef S1D_NO_LEVEL_BARRIER
+    __syncwarp();
+#else
+    __syncthreads();
+#endif
+}
 
 template <int Q>
 __device__ __forceinline__ void fpublish(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int r) {
@@ -253,7 +264,7 @@ __device__ __forceinline__ void fexpand_seg(const Fold<Q>& c, double (&vl)[Q], d
         if (INS) finsert(c, vl, vr, r);
         if (INS || CP) fpublish(c, vl, vr, r);
         feed(r);
-        S1D_LEVEL_BARRIER();
+        level_sync();
         if (CP) fcompute(c, vl, vr, r, fo);
     }
 }
@@ -278,7 +289,7 @@ __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q],
 #pragma unroll UN
     for (int r = r0; r < r1; ++r) {
         if (PB) fpublish(c, vl, vr, r);
-        S1D_LEVEL_BARRIER();
+        level_sync();
         if (CP) fcompute(c, vl, vr, r, fo);
         if (EX) fexport(c, vl, vr, r - c.m, oL, oR, live);
     }
@@ -300,8 +311,15 @@ __device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], dou
 // Shared memory (doubles): exchange 8*(tt+2)*G, then one region reused in turn:
 // ring 4*levels*G (Diamond/Down), state staging G*(w+1) (Up/Down) and, for
 // short tiles, export staging 2*G*(w+1) (Up/Diamond, after the last ring read).
+// Slots of a folded tile: ceil(m / Q) with m = w/2 distances per side and
+// Q = P/2 per slot. When Q does not divide m, the last slot's top distances
+// (>= m) are padding: outside every level's span (no export reads them) and
+// filled by the inserts' one-sided predicate; distance m itself, the halo of
+// level m, then lives in a register instead of slot tt's exchange entry.
+__host__ __device__ inline int fold_slots(int w, int P) { return (w / 2 + P / 2 - 1) / (P / 2); }
+
 __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P, int G) {
-    const std::size_t tt = (std::size_t)(w / P);
+    const std::size_t tt = (std::size_t)fold_slots(w, P);
     const std::size_t ring = kind != kUp ? 4 * (std::size_t)ring_levels(w / 2) * G : 0;
     const std::size_t stage = kind != kDiamond ? (std::size_t)G * (w + 1) : 0;
     // short tiles stage their exports ([2][G][w+1]) in the same region
@@ -319,7 +337,7 @@ template <int Q, int KIND, int MAXT, int MINB, int U, bool XS>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
     const int w = a.w, m = a.m;
-    const int tt = m / Q; // slots per tile
+    const int tt = (m + Q - 1) / Q; // slots per tile (fold_slots)
     const int nt = tt * G;
     const int t = threadIdx.x;
     const int s = t / G, g = t - s * G;
@@ -342,9 +360,10 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     const int rmask = 2 * rl - 1;
     c.rmask = rmask;
     c.err = a.error_flag;
-    double* const ringR = sm + 8 * c.xs; // [2*rl][G]
+    double* const region = sm + 8 * c.xs;
+    double* const ringR = region; // [2*rl][G]
     double* const ringL = ringR + 2 * rl * G;
-    double* const stage = ringR;         // Up/Down [G][w+1]
+    double* const stage = region;        // Up/Down [G][w+1]
     c.ringR = ringR;
     c.ringL = ringL;
     {
@@ -367,8 +386,10 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         const double* my = stage + g * ws; // core x-1: left d at m-1-d, right d at m+d
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
-            vl[k] = my[m - 1 - (s * Q + k)];
-            vr[k] = my[m + s * Q + k];
+            if (s * Q + k < m) { // padding distances stay 0
+                vl[k] = my[m - 1 - (s * Q + k)];
+                vr[k] = my[m + s * Q + k];
+            }
         }
     }
 
@@ -439,10 +460,10 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
             const int r = m;
             finsert(c, vl, vr, r);
             fpublish(c, vl, vr, r);
-            if (s == tt - 1)
+            if (s == tt - 1 && m % Q == 0) // else distance m is a register of slot tt-1 (finsert)
                 c.F[(r & 1) * c.xs + (tt + 1) * G + g] =
                     make_double2(ringR[ridx(2 * (m - 1), rmask, g, G)], ringL[ridx(2 * (m - 1) + 1, rmask, g, G)]);
-            __syncthreads();
+            level_sync();
             fcompute(c, vl, vr, r, fo);
         }
     }
@@ -474,8 +495,10 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         double* my = stage + g * ws;
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
-            my[m - 1 - (s * Q + k)] = vl[k];
-            my[m + s * Q + k] = vr[k];
+            if (s * Q + k < m) {
+                my[m - 1 - (s * Q + k)] = vl[k];
+                my[m + s * Q + k] = vr[k];
+            }
         }
         __syncthreads();
         const std::int64_t centre0 = a.seam ? (std::int64_t)(bfirst + 1) * w : (std::int64_t)bfirst * w + w / 2;
@@ -696,11 +719,11 @@ __global__ void __launch_bounds__(256) heat_tile_debug_kernel(const TileArgs a, 
     }
 }
 
-int tiles_per_cta(int w, int p) {
-    const int tt = w / p;
+int tiles_per_cta(int w, int p, int maxt = 256) {
+    const int tt = fold_slots(w, p);
     int G = 1;
-    if (tt > 256) return 1;
-    while ((G * 2) * tt <= 256 && G * 2 <= 64) G *= 2;
+    if (tt > maxt) return 1;
+    while ((G * 2) * tt <= maxt && G * 2 <= 64) G *= 2;
     return G;
 }
 
@@ -708,8 +731,9 @@ template <int P, int MAXT = 256, int MINB = 1, int U = 1, bool XS = false>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     static_assert(P % 2 == 0, "the folded layout holds P/2 distance pairs per thread");
     if (XS != (a.m <= kXportLevels)) return cudaErrorInvalidValue;
-    const int tt = a.w / P;
-    const int G = tiles_per_cta(a.w, P);
+    const int tt = fold_slots(a.w, P);
+    if (tt > MAXT) return cudaErrorInvalidValue;
+    const int G = tiles_per_cta(a.w, P, MAXT);
     const int nt = G * tt;
     const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
     void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS>
@@ -731,24 +755,25 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
 int heat_points_per_thread(int w, long long tiles) {
     if (const char* e = std::getenv("S1D_HEAT_P")) {
         const int p = std::atoi(e);
-        if ((p == 2 || p == 4 || p == 8 || p == 16) && w % p == 0 && w / p <= 256) return p;
+        if ((p == 2 || p == 4 || p == 8 || p == 16) && fold_slots(w, p) <= 256) return p;
     }
-    // Folded layout: P even (P/2 distance pairs per thread). Measured on B200
-    // (n = 2^27, each with its register cap / unroll): P = 16 from w = 128
-    // (twice the work per level barrier of P = 8: +9% at w = 1024), P = 8 at
-    // w = 32..64 or when 16 does not divide w, else P = 4; wide tiles double P
-    // until w/P <= 256 threads. Always P | w, w/P <= 256 except for w = 2 mod 4
-    // (P = 2, up to 1024 threads).
+    // Folded layout: P even (P/2 distance pairs per thread), ceil(m / (P/2))
+    // slots (fold_slots: a ragged last slot pads). Measured on B200 (n = 2^27,
+    // each with its register cap / unroll): P = 16 from w = 128 (twice the
+    // work per level barrier of P = 8: +9% at w = 1024; w = 1000, padded:
+    // 1.75 T vs 1.60 T with P = 8), except 128 < w < 256 when 16 does not
+    // divide w (w = 200: P = 8 1.46 T, padded P = 16 1.37 T); P = 8 at
+    // w = 32..127; narrower tiles P = 4 (w = 0 mod 4) or 2. Tiles wider than
+    // 256 slots run P = 16 in CTAs of up to 1024 threads (w <= 16384).
     int p = 2;
-    if (w % 16 == 0 && w >= 128) p = 16;
-    else if (w % 8 == 0 && w >= 32) p = 8;
+    if (w >= 256 || (w >= 128 && w % 16 == 0)) p = 16;
+    else if (w >= 32) p = 8;
     else if (w % 4 == 0) p = 4;
-    while (w / p > 256 && w % (2 * p) == 0 && p < 16) p *= 2;
-    if (w / p > 1024) return -1; // no valid decomposition (caller reports it)
+    if (fold_slots(w, p) > 1024) return -1; // no valid decomposition (caller reports it)
     // Small grids: P = 16 packs twice the tiles per CTA of P = 8; below one
     // full wave (4 CTAs per SM) P = 8 fills the GPU better (measured n = 2^20:
     // 1.29-1.32 T with P = 8 vs 1.01-1.04 T with P = 16 at w = 256..1024).
-    if (p == 16 && tiles >= 0 && w / 8 <= 256) {
+    if (p == 16 && tiles >= 0 && fold_slots(w, 8) <= 256) {
         static int sms = 0;
         if (sms == 0) {
             int dev = 0;
@@ -766,11 +791,8 @@ int heat_points_per_thread(int w, long long tiles) {
 
 cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st) {
     const std::uint64_t pairs = a.N >> 1;
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     std::uint64_t blocks = (pairs + 255) / 256;
-    const std::uint64_t cap = (std::uint64_t)sms * 8 * 4;
+    const std::uint64_t cap = (std::uint64_t)a.sms * 8 * 4;
     if (blocks > cap) blocks = cap;
     if (blocks == 0) blocks = 1;
     heat_classic_kernel<<<(unsigned)blocks, 256, 0, st>>>(a);
@@ -796,18 +818,23 @@ cudaError_t launch_tile_debug(int kind, const TileArgs& a, cudaStream_t st) {
 }
 
 cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool debug) {
-    if (a.w % a.p || a.w / a.p > 1024) return cudaErrorInvalidValue;
     if (debug) {
-        if (a.w / a.p > 256) return cudaErrorInvalidValue;
-        switch (a.p) {
-        case 2: return launch_tile_debug<2>(kind, a, st);
-        case 4: return launch_tile_debug<4>(kind, a, st);
-        case 8: return launch_tile_debug<8>(kind, a, st);
-        case 16: return launch_tile_debug<16>(kind, a, st);
-        default: return cudaErrorInvalidValue;
+        // the instrumented kernel's contiguous layout needs P | w, w/P <= 256
+        for (int p : {16, 8, 4, 2}) {
+            if (a.w % p || a.w / p > 256) continue;
+            switch (p) {
+            case 2: return launch_tile_debug<2>(kind, a, st);
+            case 4: return launch_tile_debug<4>(kind, a, st);
+            case 8: return launch_tile_debug<8>(kind, a, st);
+            default: return launch_tile_debug<16>(kind, a, st);
+            }
         }
+        return cudaErrorInvalidValue;
     }
-    if (a.w / a.p > 256) return a.p == 2 ? launch_tile_p<2, 1024>(kind, a, st) : cudaErrorInvalidValue;
+    const int slots = fold_slots(a.w, a.p);
+    if (slots > 1024) return cudaErrorInvalidValue;
+    if (slots > 256) // very wide tiles: one tile per CTA of up to 1024 threads
+        return a.p == 16 ? launch_tile_p<16, 1024>(kind, a, st) : cudaErrorInvalidValue;
     const bool xs = a.m <= kXportLevels; // short tiles: staged exports (XS build)
     switch (a.p) {
     case 2: return xs ? launch_tile_p<2, 256, 1, 1, true>(kind, a, st) : launch_tile_p<2>(kind, a, st);
@@ -818,7 +845,8 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
         return xs ? launch_tile_p<8, 256, 4, 2, true>(kind, a, st) : launch_tile_p<8, 256, 4, 2>(kind, a, st);
     case 16: // measured (n = 2^27): 4 CTAs/SM + unroll 2 from w = 256 (1.95-1.97 T), 3 CTAs/SM at w = 128
         if (xs) return launch_tile_p<16, 256, 1, 1, true>(kind, a, st);
-        return a.w >= 256 ? launch_tile_p<16, 256, 4, 2>(kind, a, st) : launch_tile_p<16, 256, 3, 1>(kind, a, st);
+        if (a.w < 256) return launch_tile_p<16, 256, 3, 1>(kind, a, st);
+        return launch_tile_p<16, 256, 4, 2>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
 }

@@ -49,6 +49,8 @@ struct TileArgs {
     // physics
     double fourier = 0.4, gamma = 1.4, dt_dx = 0.0;
     int* error_flag = nullptr;      // device NonPhysicalState flag (Euler)
+    double* scratch = nullptr;      // Euler tiles too wide for shared memory: per-CTA records (launcher-owned)
+    int sms = 148;                  // SMs of the launching device (queried once per shard, not per launch)
     DebugArgs dbg;
 };
 
@@ -81,6 +83,7 @@ struct ClassicArgs {
     unsigned* sig_left = nullptr;
     unsigned* sig_right = nullptr;
     unsigned long long timeout_ns = 0;
+    int sms = 148;                  // SMs of the launching device (queried once per shard)
 };
 
 // `debug` selects the instrumented instantiation (coverage / perturb).

@@ -59,8 +59,11 @@ def test_decomp_cases(gpu, scheme, c):
             assert res.stats.bytes_sent == c["classic_bytes"]
 
 
+# 3000 and 4096: tiles beyond a CTA's shared memory (records in global
+# scratch); the reference's check_width has no upper bound
+# (R/core/src/swept.cpp:10-19)
 @pytest.mark.parametrize("method", ["lengthening", "flattening"])
-@pytest.mark.parametrize("w", [8, 12, 16, 32, 64, 128, 256, 512, 1024])
+@pytest.mark.parametrize("w", [8, 12, 16, 32, 64, 128, 256, 512, 1024, 2048, 3000, 4096])
 def test_width_sweep_unaligned(gpu, method, w):
     h = 1 if method == "lengthening" else 2
     S = 4 if method == "lengthening" else 2

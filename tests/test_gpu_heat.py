@@ -49,7 +49,12 @@ def test_decomp_cases(gpu, n, w, ranks, wf, steps, scheme):
         assert_bitwise(got, want)
 
 
-@pytest.mark.parametrize("w", [4, 6, 8, 12, 16, 32, 64, 128, 256, 512, 514, 1000, 1024, 2048, 4096])
+# incl. widths whose half-width the slot size does not divide (ragged last
+# slot: 34, 200, 514, 1000, 2050) and beyond 256 slots (2050, 4100, 8192:
+# CTAs of up to 1024 threads); the reference's check_width has no upper
+# bound (R/core/src/swept.cpp:10-19)
+@pytest.mark.parametrize("w", [4, 6, 8, 12, 16, 32, 34, 64, 128, 200, 256, 512, 514, 1000, 1024, 2048, 2050, 4096,
+                               4100, 8192])
 def test_width_sweep_unaligned(gpu, w):
     n = max(4 * w, 1 << 13)
     n -= n % w

@@ -14,6 +14,7 @@ def main():
         n = 1 << lg
         for scheme in (s1d.Scheme.Classic, s1d.Scheme.Swept):
             for w in ws if scheme == s1d.Scheme.Swept else ws[:1]:
+                n = (1 << lg) // w * w  # a whole number of tiles
                 c = s1d.LaunchConfig(equation=s1d.Equation.Heat if eq == "heat" else s1d.Equation.Euler,
                                      scheme=scheme, grid_size=n, block_width=w, ranks=1, steps=steps)
                 with s1d.Solver(c) as sv:
