@@ -85,7 +85,7 @@ typedef struct s1d_config {
     double gamma;           /*     (default 1.4) */
     double dt_dx;           /* 0 = derived from cfl at finalize (Euler) */
     double cfl;             /*     (default 0.4) */
-    double alpha, beta, compute_cost; /* transport cost model: accepted, unused */
+    double alpha, beta, compute_cost; /* transport cost model (virtual mode, CommStats::virtual_comm_time) */
     char initial[64];       /* "" = per-equation default */
     int num_devices;        /* 0 = all visible devices */
     int reserved[7];
@@ -105,13 +105,31 @@ typedef struct s1d_stats {
                                     alpha + beta*bytes over rounds (any mode) */
 } s1d_stats;
 
+/* RankCommStats (inc/transport.hpp:17-25): one rank's counters. */
+typedef struct s1d_rank_stats {
+    uint64_t messages_sent;
+    uint64_t bytes_sent;
+    uint64_t exchange_rounds;
+    double virtual_comm_seconds;
+} s1d_rank_stats;
+
+/* MessageLogEntry (inc/transport.hpp:36-42): one message of the reference
+ * transport's log (RunOptions::keep_message_log). */
+typedef struct s1d_message {
+    uint64_t round;
+    int32_t source;
+    int32_t dest;
+    uint64_t tag;
+    uint64_t bytes;
+} s1d_message;
+
 /* EngineTiming (inc/engine.hpp:12-16). loop_seconds = max over shards of the
  * CUDA-event time of the stepping loop (setup and host copies excluded);
  * h2d/d2h seconds are reported separately. */
 typedef struct s1d_timing {
     double setup_seconds;
     double loop_seconds;
-    double virtual_seconds; /* always 0 */
+    double virtual_seconds; /* virtual mode: the reference's alpha-beta clock (s1d_virtual_time) */
     double h2d_seconds;
     double d2h_seconds;
     /* The dominant kernel of the run (swept: the Diamond phases; classic: the
@@ -145,6 +163,12 @@ int s1d_max_signal_speed(const double* prim, size_t len, double gamma, double* o
 int s1d_partition(const s1d_config* cfg, uint64_t* blocks, uint64_t* start_index, int* left, int* right,
                   char* err, size_t errlen);
 int64_t s1d_cycle_advance(uint64_t w, uint64_t h, char* err, size_t errlen); /* <0: -status */
+/* The message log RunResult::log holds for cfg with keep_message_log
+ * (RingTransport::sorted_log, transport.cpp:197-206): *count = its length, up
+ * to cap entries written. Payload sizes are the reference's Cell bytes. */
+int s1d_message_log(const s1d_config* cfg, s1d_message* out, size_t cap, size_t* count, char* err, size_t errlen);
+/* CommStats::per_rank for cfg (transport.cpp:190-196); arrays of cfg->ranks. */
+int s1d_comm_per_rank(const s1d_config* cfg, s1d_rank_stats* out, size_t cap, char* err, size_t errlen);
 /* kind 0 triangle, 1 diamond, 2 down-triangle. Returns the level count (or
  * -status); fills up to cap (substep, lo, hi) triples. */
 int64_t s1d_schedule(int kind, uint64_t w, uint64_t h, int64_t* substep, int64_t* lo, int64_t* hi, size_t cap,

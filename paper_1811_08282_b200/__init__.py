@@ -17,3 +17,4 @@ from .api import (  # noqa: F401
     read_csv, speedup)
 from .api import DebugResult, RunOptions, run_debug  # noqa: F401
 from .api import calibrate_transport, virtual_time  # noqa: F401
+from .api import MessageLogEntry, RankCommStats, message_log, rank_stats  # noqa: F401

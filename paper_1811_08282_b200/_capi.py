@@ -33,6 +33,16 @@ class s1d_stats(C.Structure):
                 ("virtual_comm_seconds", C.c_double)]
 
 
+class s1d_rank_stats(C.Structure):
+    _fields_ = [("messages_sent", C.c_uint64), ("bytes_sent", C.c_uint64), ("exchange_rounds", C.c_uint64),
+                ("virtual_comm_seconds", C.c_double)]
+
+
+class s1d_message(C.Structure):
+    _fields_ = [("round", C.c_uint64), ("source", C.c_int32), ("dest", C.c_int32), ("tag", C.c_uint64),
+                ("bytes", C.c_uint64)]
+
+
 class s1d_timing(C.Structure):
     _fields_ = [("setup_seconds", C.c_double), ("loop_seconds", C.c_double), ("virtual_seconds", C.c_double),
                 ("h2d_seconds", C.c_double), ("d2h_seconds", C.c_double), ("dominant_seconds", C.c_double),
@@ -91,6 +101,9 @@ SIGNATURES = {
     "s1d_last_error": (C.c_char_p, [C.c_void_p]),
     "s1d_measure_fp64_peak": (C.c_int, [C.c_int, C.POINTER(C.c_double)] + _E),
     "s1d_virtual_time": (C.c_int, [C.POINTER(s1d_config), _dp, _dp] + _E),
+    "s1d_message_log": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_message), C.c_size_t,
+                                  C.POINTER(C.c_size_t)] + _E),
+    "s1d_comm_per_rank": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_rank_stats), C.c_size_t] + _E),
     "s1d_calibrate_transport": (C.c_int, [C.c_int, C.c_int, _dp, _dp] + _E),
     "s1d_measure": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_record)] + _E),
     "s1d_csv_header": (C.c_char_p, []),

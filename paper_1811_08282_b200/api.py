@@ -386,6 +386,25 @@ def down_triangle_schedule(w: int, h: int) -> PhaseSchedule:
 # run (engine.hpp:12-28)
 # ---------------------------------------------------------------------------
 @dataclass
+class RankCommStats:
+    """RankCommStats (inc/transport.hpp:17-25)."""
+    messages_sent: int = 0
+    bytes_sent: int = 0
+    exchange_rounds: int = 0
+    virtual_comm_time: float = 0.0
+
+
+@dataclass
+class MessageLogEntry:
+    """MessageLogEntry (inc/transport.hpp:36-42)."""
+    round: int
+    source: int
+    dest: int
+    tag: int
+    bytes: int
+
+
+@dataclass
 class CommStats:
     messages_sent: int = 0
     bytes_sent: int = 0
@@ -394,6 +413,7 @@ class CommStats:
     edge_bytes_device: int = 0
     setup_seconds: float = 0.0
     virtual_comm_time: float = 0.0  # CommStats::virtual_comm_time (transport.hpp:20-30)
+    per_rank: list = field(default_factory=list)  # [RankCommStats] (transport.cpp:190-196)
 
 
 @dataclass
@@ -451,19 +471,48 @@ def _out_buffer(out: Optional[np.ndarray], n: int) -> np.ndarray:
     return out
 
 
-def run(cfg: LaunchConfig) -> RunResult:
-    """The drop-in for sweep1d::run (src/engine.cpp:40-47) on B200 GPUs."""
-    spec = cfg.spec()
-    out = np.empty(cfg.grid_size * spec.values_per_point, dtype=np.float64)
-    st, tm = _capi.s1d_stats(), _capi.s1d_timing()
+def run(cfg: LaunchConfig, opts: Optional["RunOptions"] = None) -> RunResult:
+    """The drop-in for sweep1d::run(cfg, opts) (src/engine.cpp:40-47) on B200
+    GPUs. stats.per_rank and (opts.keep_message_log) the log are the
+    reference transport's, replayed on the host (rank_stats, message_log)."""
+    if opts is not None and (opts.coverage or opts.perturb_ulp):
+        res = run_debug(cfg, opts).result
+    else:
+        spec = cfg.spec()
+        out = np.empty(cfg.grid_size * spec.values_per_point, dtype=np.float64)
+        st, tm = _capi.s1d_stats(), _capi.s1d_timing()
+        e = _errbuf()
+        _check(lib().s1d_run(C.byref(cfg.to_c()), _dptr(out), out.size, C.byref(st), C.byref(tm), e, 1024), e)
+        res = RunResult(out, _stats(st, tm.setup_seconds), _timing(tm))
+    res.stats.per_rank = rank_stats(cfg)
+    if opts is not None and opts.keep_message_log:
+        res.log = message_log(cfg)
+    return res
+
+
+def rank_stats(cfg: LaunchConfig) -> list:
+    """CommStats::per_rank for cfg (transport.cpp:190-196), host-only."""
+    arr = (_capi.s1d_rank_stats * max(cfg.ranks, 1))()
     e = _errbuf()
-    _check(lib().s1d_run(C.byref(cfg.to_c()), _dptr(out), out.size, C.byref(st), C.byref(tm), e, 1024), e)
-    return RunResult(out, _stats(st, tm.setup_seconds), _timing(tm))
+    _check(lib().s1d_comm_per_rank(C.byref(cfg.to_c()), arr, len(arr), e, 1024), e)
+    return [RankCommStats(a.messages_sent, a.bytes_sent, a.exchange_rounds, a.virtual_comm_seconds) for a in arr]
+
+
+def message_log(cfg: LaunchConfig) -> list:
+    """The reference transport's sorted message log for cfg
+    (RunOptions::keep_message_log; transport.cpp:66-110, 197-206), host-only."""
+    n = C.c_size_t(0)
+    e = _errbuf()
+    _check(lib().s1d_message_log(C.byref(cfg.to_c()), None, 0, C.byref(n), e, 1024), e)
+    arr = (_capi.s1d_message * max(n.value, 1))()
+    _check(lib().s1d_message_log(C.byref(cfg.to_c()), arr, n.value, C.byref(n), e, 1024), e)
+    return [MessageLogEntry(m.round, m.source, m.dest, m.tag, m.bytes) for m in arr[:n.value]]
 
 
 @dataclass
 class RunOptions:
-    """sweep1d::RunOptions subset (inc/debug.hpp:17-24) for instrumented runs."""
+    """sweep1d::RunOptions subset (inc/debug.hpp:17-24)."""
+    keep_message_log: bool = False
     coverage: bool = False
     perturb_ulp: bool = False
 

@@ -55,6 +55,7 @@ struct Shard {
     double* EL[2] = {nullptr, nullptr};
     double* ER[2] = {nullptr, nullptr};
     unsigned* flags = nullptr; // multi-process: [0] left neighbour's rounds, [1] right's
+    int* fallback = nullptr;   // heat tiles: per-CTA verdict of the fast build (heat.cu heat_step)
     unsigned* cov = nullptr;   // debug runs: coverage counts [total][n]
     cudaStream_t cs = nullptr; // copy stream for pipelined host I/O (s1d_solve)
     std::vector<cudaEvent_t> ev_h2d, ev_dn; // per I/O chunk
@@ -79,6 +80,13 @@ struct ShardBlob {
 // Dead-peer guard of the device-side round waits (sticky: only the first
 // wait after a peer died pays it). 60 s by default; S1D_ROUND_TIMEOUT_S
 // overrides it (read once per process).
+// Kernel launches of one tile phase: the heat fast build is followed by its
+// gated exact build (heat.cu heat_step) when 0 <= Fo <= 0.5.
+int heat_tile_launches(bool euler, bool debug, const TileArgs& a) {
+    if (euler || debug) return 1;
+    return a.fallback && a.fourier >= 0.0 && a.fourier <= 0.5 ? 2 : 1;
+}
+
 // SM count of a device (grid sizing), cached per device.
 int device_sms(int dev) {
     static int cache[64] = {};
@@ -171,6 +179,7 @@ struct Solver {
                 cudaFree(s.ER[k]);
             }
             cudaFree(s.flags);
+            cudaFree(s.fallback);
             cudaFree(s.cov);
             cudaFree(s.err);
             cudaFree(s.staging);
@@ -255,6 +264,8 @@ struct Solver {
                 S1D_CUDA(cudaMalloc(&s.EL[k], edge_bytes));
                 S1D_CUDA(cudaMalloc(&s.ER[k], edge_bytes));
             }
+            if (!euler) // heat tile kernels: per-CTA fast/exact verdicts (one per tile bounds any grid)
+                S1D_CUDA(cudaMalloc(&s.fallback, sizeof(int) * (s.nb + 1)));
         }
         if (mp) {
             S1D_CUDA(cudaMalloc(&s.flags, 256));
@@ -698,12 +709,13 @@ struct Solver {
             a.dt_dx = cfg.dt_dx;
             a.error_flag = s.err;
             a.sms = s.sms;
+            a.fallback = s.fallback;
             a.dbg = dbg_args(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             auto launch = [&](const TileArgs& ta) {
                 if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, ta, s.st, debug));
                 else S1D_CUDA(launch_heat_tile(kind, ta, s.st, debug));
-                stats.kernel_launches += 1;
+                stats.kernel_launches += heat_tile_launches(euler, debug, ta);
             };
             if (pio && (kind == kUp || kind == kDown)) {
                 const int K = pio->K;
@@ -1111,6 +1123,31 @@ int64_t s1d_cycle_advance(uint64_t w, uint64_t h, char* err, size_t errlen) {
     std::uint64_t m = 0;
     const int st = guarded(err, errlen, [&] { m = s1d::cycle_advance(w, h); });
     return st == S1D_OK ? static_cast<int64_t>(m) : -st;
+}
+
+int s1d_message_log(const s1d_config* cfg, s1d_message* out, size_t cap, size_t* count, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        need(cfg, "config");
+        need(count, "count");
+        if (cap && !out) need(out, "out");
+        s1d_config c = *cfg;
+        s1d::finalize(c, true);
+        const auto log = s1d::message_log(c);
+        *count = log.size();
+        for (std::size_t i = 0; i < log.size() && i < cap; ++i) out[i] = log[i];
+    });
+}
+
+int s1d_comm_per_rank(const s1d_config* cfg, s1d_rank_stats* out, size_t cap, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        need(cfg, "config");
+        need(out, "out");
+        s1d_config c = *cfg;
+        s1d::finalize(c, true);
+        const auto st = s1d::rank_stats(c);
+        if (cap < st.size()) throw s1d::Error(S1D_INVALID_CONFIG, "output buffer too small");
+        for (std::size_t i = 0; i < st.size(); ++i) out[i] = st[i];
+    });
 }
 
 int s1d_virtual_time(const s1d_config* cfg, double* virtual_seconds, double* comm_seconds, char* err,

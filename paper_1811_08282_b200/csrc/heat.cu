@@ -40,12 +40,32 @@ namespace s1d {
 namespace {
 
 __device__ __forceinline__ double heat_f(double l, double c, double r, double fo) {
-#ifdef S1D_EXP_FMA
-    return __dadd_rn(c, __dmul_rn(fo, __dadd_rn(__fma_rn(-2.0, c, l), r)));
-#else
     return __dadd_rn(c, __dmul_rn(fo, __dadd_rn(__dsub_rn(l, __dmul_rn(2.0, c)), r)));
-#endif
 }
+
+// The tile kernels' fast form: 4 FP64 instructions instead of 5, bit for bit
+// the same result whenever 2c does not overflow. 2c is exact (a power-of-two
+// scaling; subnormals included), so l - 2c rounded once (the reference's
+// separately rounded sub of an exact product) equals fma(-2, c, l) rounded
+// once; signed zeros agree (checked case by case), and infinities/NaNs
+// propagate alike. The only difference is |c| >= 2^1023, where 2c overflows
+// to inf in the reference but not inside the fma. The tile kernels therefore
+// use this form only when no value of the launch can reach 2^1023: with
+// 0 <= Fo <= 0.5 each FTCS step is a convex combination, so
+// |T'| <= max(|l|,|c|,|r|) * (1 + 7*2^-53) after rounding, and a launch of at
+// most 2m <= 16384 levels whose inputs (state or producer edges) all satisfy
+// |v| < 2^1022 keeps every value below 2^1022 * (1 + 2^-35) < 2^1023
+// (intermediates: |l - 2c| <= 3M, |(l - 2c) + r| <= 4M < 2^1024). Any other
+// launch (a NaN/inf or |v| >= 2^1022 input, or Fo outside [0, 0.5]) runs
+// heat_f. The check reads every input once (tile_inputs_fit).
+template <bool FU>
+__device__ __forceinline__ double heat_step(double l, double c, double r, double fo) {
+    if (FU) return __dadd_rn(c, __dmul_rn(fo, __dadd_rn(__fma_rn(-2.0, c, l), r)));
+    return heat_f(l, c, r, fo);
+}
+
+// |v| >= 2^1022, inf or NaN (biased exponent >= 0x7fd)
+__device__ __forceinline__ bool too_big(double v) { return (__double2hiint(v) & 0x7fffffff) >= 0x7fd00000; }
 
 __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) {
     // Two points per thread (N is a multiple of the even block width). Only the
@@ -186,7 +206,7 @@ __device__ __forceinline__ void fpublish(const Fold<Q>& c, const double (&vl)[Q]
     c.Lst[i] = make_double2(vl[Q - 1], vr[Q - 1]);
 }
 
-template <int Q>
+template <int Q, bool FU>
 __device__ __forceinline__ void fcompute(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r, double fo) {
     const int par = (r & 1) * c.xs;
     const double2 in = c.Lst[par + c.s * c.G + c.g];      // slot s-1: distance sQ-1
@@ -198,9 +218,9 @@ __device__ __forceinline__ void fcompute(const Fold<Q>& c, double (&vl)[Q], doub
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
         // right x = w/2+1+d: (x-1, x, x+1) = distances (d-1, d, d+1)
-        nr[k] = heat_f(k == 0 ? inR : vr[k - 1], vr[k], k == Q - 1 ? out.y : vr[k + 1], fo);
+        nr[k] = heat_step<FU>(k == 0 ? inR : vr[k - 1], vr[k], k == Q - 1 ? out.y : vr[k + 1], fo);
         // left x = w/2-d: (x-1, x, x+1) = distances (d+1, d, d-1)
-        nl[k] = heat_f(k == Q - 1 ? out.x : vl[k + 1], vl[k], k == 0 ? inL : vl[k - 1], fo);
+        nl[k] = heat_step<FU>(k == Q - 1 ? out.x : vl[k + 1], vl[k], k == 0 ? inL : vl[k - 1], fo);
     }
 #pragma unroll
     for (int k = 0; k < Q; ++k) {
@@ -255,7 +275,7 @@ __device__ __forceinline__ void fexport(const Fold<Q>& c, const double (&vl)[Q],
 // the loops contain barriers; `live` only predicates stores).
 // U: unroll of the long compute-only segments (lets the compiler rename the
 // loop-carried registers instead of copying them; measured per width).
-template <int Q, int U, bool INS, bool CP, class Feed>
+template <int Q, int U, bool FU, bool INS, bool CP, class Feed>
 __device__ __forceinline__ void fexpand_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                             double fo, Feed& feed) {
     constexpr int UN = (!INS && CP) ? U : 1;
@@ -265,24 +285,24 @@ __device__ __forceinline__ void fexpand_seg(const Fold<Q>& c, double (&vl)[Q], d
         if (INS || CP) fpublish(c, vl, vr, r);
         feed(r);
         level_sync();
-        if (CP) fcompute(c, vl, vr, r, fo);
+        if (CP) fcompute<Q, FU>(c, vl, vr, r, fo);
     }
 }
 
 // Expanding levels [r0, r1), span distances [0, r): idle below sa*Q, insert
 // while r in [sa*Q, (sb+1)*Q], compute from sa*Q + 1.
-template <int Q, int U, class Feed>
+template <int Q, int U, bool FU, class Feed>
 __device__ __forceinline__ void fexpand(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                         double fo, Feed& feed) {
     const int a = c.sa * Q, bi = (c.sb + 1) * Q + 1;
     const int e0 = min(max(a, r0), r1), e1 = min(max(a + 1, r0), r1), e2 = min(max(bi, r0), r1);
-    fexpand_seg<Q, U, false, false>(c, vl, vr, r0, e0, fo, feed);
-    fexpand_seg<Q, U, true, false>(c, vl, vr, e0, e1, fo, feed);
-    fexpand_seg<Q, U, true, true>(c, vl, vr, e1, e2, fo, feed);
-    fexpand_seg<Q, U, false, true>(c, vl, vr, e2, r1, fo, feed);
+    fexpand_seg<Q, U, FU, false, false>(c, vl, vr, r0, e0, fo, feed);
+    fexpand_seg<Q, U, FU, true, false>(c, vl, vr, e0, e1, fo, feed);
+    fexpand_seg<Q, U, FU, true, true>(c, vl, vr, e1, e2, fo, feed);
+    fexpand_seg<Q, U, FU, false, true>(c, vl, vr, e2, r1, fo, feed);
 }
 
-template <int Q, int U, bool PB, bool CP, bool EX>
+template <int Q, int U, bool FU, bool PB, bool CP, bool EX>
 __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                               double fo, double* oL, double* oR, bool live) {
     constexpr int UN = (PB && CP && !EX) ? U : 1;
@@ -290,22 +310,22 @@ __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q],
     for (int r = r0; r < r1; ++r) {
         if (PB) fpublish(c, vl, vr, r);
         level_sync();
-        if (CP) fcompute(c, vl, vr, r, fo);
+        if (CP) fcompute<Q, FU>(c, vl, vr, r, fo);
         if (EX) fexport(c, vl, vr, r - c.m, oL, oR, live);
     }
 }
 
 // Contracting levels [r0, r1), r = m+d, span distances [0, m-d): compute
 // while r <= 2m-1-sa*Q, export from 2m-1-(sb+1)*Q on, publish one level longer.
-template <int Q, int U>
+template <int Q, int U, bool FU>
 __device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                           double fo, double* oL, double* oR, bool live) {
     const int rce = 2 * c.m - 1 - c.sa * Q, ae = 2 * c.m - 1 - (c.sb + 1) * Q;
     const int e0 = min(max(ae, r0), r1), e1 = min(max(rce + 1, r0), r1), e2 = min(max(rce + 2, r0), r1);
-    fcontract_seg<Q, U, true, true, false>(c, vl, vr, r0, e0, fo, oL, oR, live);
-    fcontract_seg<Q, U, true, true, true>(c, vl, vr, e0, e1, fo, oL, oR, live);
-    fcontract_seg<Q, U, true, false, false>(c, vl, vr, e1, e2, fo, oL, oR, live);
-    fcontract_seg<Q, U, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
+    fcontract_seg<Q, U, FU, true, true, false>(c, vl, vr, r0, e0, fo, oL, oR, live);
+    fcontract_seg<Q, U, FU, true, true, true>(c, vl, vr, e0, e1, fo, oL, oR, live);
+    fcontract_seg<Q, U, FU, true, false, false>(c, vl, vr, e1, e2, fo, oL, oR, live);
+    fcontract_seg<Q, U, FU, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
 }
 
 // Shared memory (doubles): exchange 8*(tt+2)*G, then one region reused in turn:
@@ -333,9 +353,10 @@ __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P,
 // spills; measured +4-10% over the uncapped build).
 // XS: short-tile build (m <= kXportLevels): cp.async ring init and staged
 // exports; wide tiles instantiate XS = false (code identical to before).
-template <int Q, int KIND, int MAXT, int MINB, int U, bool XS>
+template <int Q, int KIND, int MAXT, int MINB, int U, bool XS, bool FU>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
+    if (!FU && a.fallback && a.fallback[blockIdx.x] == 0) return; // the fast build did this CTA
     const int w = a.w, m = a.m;
     const int tt = (m + Q - 1) / Q; // slots per tile (fold_slots)
     const int nt = tt * G;
@@ -376,13 +397,24 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
 #pragma unroll
     for (int k = 0; k < Q; ++k) vl[k] = vr[k] = 0.0;
 
+    // FU (fast form, heat_step<true>): only if every input of this CTA's
+    // tiles is below 2^1022 (see heat_step; the launcher guarantees
+    // 0 <= Fo <= 0.5): the Up kernel's state, the Diamond/Down kernels'
+    // producer edges (re-read once here: a few GB/s next to the FP64-bound
+    // level loop). A CTA that finds a larger input writes nothing, records
+    // it in a.fallback, and the exact build (FU = false, gated on that
+    // record) computes its tiles in the same stream right after.
+    bool big = false;
     if (KIND == kUp) { // coalesced staging of the CTA's ntiles*w contiguous points
         const double* src = a.state_in + (std::size_t)bfirst * w;
         for (int j = t; j < ntiles * w; j += nt) {
             const int gg = j / w;
-            stage[gg * ws + (j - gg * w)] = src[j];
+            const double v = src[j];
+            if (FU) big |= too_big(v);
+            stage[gg * ws + (j - gg * w)] = v;
         }
-        __syncthreads();
+        if (FU) big = __syncthreads_or(big);
+        else __syncthreads();
         const double* my = stage + g * ws; // core x-1: left d at m-1-d, right d at m+d
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
@@ -454,8 +486,20 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     double* oL = a.out_L + (std::size_t)b * w;
     double* oR = a.out_R + (std::size_t)b * w;
 
+    if (FU && KIND != kUp) { // producer edges: w values per side and tile
+        for (int j = t; j < ntiles * w; j += nt) {
+            const int gg = j / w, i = j - gg * w;
+            big |= too_big(srcR(bfirst + gg)[i]) | too_big(srcL(bfirst + gg)[i]);
+        }
+        big = __syncthreads_or(big);
+    }
+    if (FU) { // this CTA's verdict for the gated exact launch that follows
+        if (t == 0) a.fallback[blockIdx.x] = big ? 1 : 0;
+        if (big) return; // nothing written yet
+    }
+
     if (KIND != kUp) {
-        fexpand<Q, U>(c, vl, vr, 1, m, fo, feed);
+        fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
         { // level m: full span; the halo pair (x = 0, w+1) is distance m
             const int r = m;
             finsert(c, vl, vr, r);
@@ -464,7 +508,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
                 c.F[(r & 1) * c.xs + (tt + 1) * G + g] =
                     make_double2(ringR[ridx(2 * (m - 1), rmask, g, G)], ringL[ridx(2 * (m - 1) + 1, rmask, g, G)]);
             level_sync();
-            fcompute(c, vl, vr, r, fo);
+            fcompute<Q, FU>(c, vl, vr, r, fo);
         }
     }
     if (KIND != kDown) {
@@ -479,7 +523,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         double* eL = sx ? xL + g * ws : oL;
         double* eR = sx ? xR + g * ws : oR;
         fexport(c, vl, vr, 0, eL, eR, live);
-        fcontract<Q, U>(c, vl, vr, m + 1, 2 * m, fo, eL, eR, live);
+        fcontract<Q, U, FU>(c, vl, vr, m + 1, 2 * m, fo, eL, eR, live);
         if (sx) {
             __syncthreads();
             double* gL = a.out_L + (std::size_t)bfirst * w;
@@ -736,18 +780,32 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     const int G = tiles_per_cta(a.w, P, MAXT);
     const int nt = G * tt;
     const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
-    void (*k)(const TileArgs, int) = kind == kUp ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS>
-                                     : kind == kDiamond ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS>
-                                                        : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS>;
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
-    }
     const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
     if (count <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((count + G - 1) / G);
-    k<<<grid, nt, smem, st>>>(a, G);
-    return cudaGetLastError();
+    // fast build + gated exact build when 0 <= Fo <= 0.5 (heat_step), else
+    // the exact build alone
+    const bool fast = a.fallback && a.fourier >= 0.0 && a.fourier <= 0.5;
+    for (int pass = fast ? 0 : 1; pass < 2; ++pass) {
+        const bool fu = pass == 0;
+        void (*k)(const TileArgs, int) =
+            kind == kUp ? (fu ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, true>
+                              : heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, false>)
+            : kind == kDiamond ? (fu ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, true>
+                                     : heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, false>)
+                               : (fu ? heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, true>
+                                     : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, false>);
+        if (smem > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            if (e != cudaSuccess) return e;
+        }
+        TileArgs ka = a;
+        if (!fast) ka.fallback = nullptr; // ungated
+        k<<<grid, nt, smem, st>>>(ka, G);
+        const cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
 }
 
 } // namespace

@@ -62,4 +62,9 @@ std::vector<Level> schedule(int kind, std::uint64_t w, std::uint64_t h);
 // returns the final max rank clock; *comm_seconds = per-rank sum of round costs.
 double virtual_clock(const s1d_config& cfg, double* comm_seconds);
 
+// The reference transport's sorted message log and per-rank counters for a
+// config (host_model.cpp).
+std::vector<s1d_message> message_log(const s1d_config& cfg);
+std::vector<s1d_rank_stats> rank_stats(const s1d_config& cfg);
+
 } // namespace s1d

@@ -51,6 +51,7 @@ struct TileArgs {
     int* error_flag = nullptr;      // device NonPhysicalState flag (Euler)
     double* scratch = nullptr;      // Euler tiles too wide for shared memory: per-CTA records (launcher-owned)
     int sms = 148;                  // SMs of the launching device (queried once per shard, not per launch)
+    int* fallback = nullptr;        // heat: per-CTA verdicts of the fast build (>= grid ints; null: exact only)
     DebugArgs dbg;
 };
 

@@ -145,3 +145,44 @@ def test_pipelined_solve_matches_oracle(gpu, eq, method, n, w, steps):
         x = O.port_initial_condition("uniform", n, eq)
         got, _, _ = sv.solve(x)
         assert_bitwise(got, x)
+
+
+# The tile kernels' fast point update (fma(-2, c, l) for l - 2c, heat.cu
+# heat_step) is exact unless 2c overflows; it runs only when 0 <= Fo <= 0.5
+# and every input of a CTA is below 2^1022, else that CTA's tiles are redone
+# by the exact build in the same stream. These cases drive each branch and
+# compare with the oracle bit for bit (NaNs compared as NaNs: their payloads
+# are platform-defined).
+def _solve(u0, w, steps, fo=0.4):
+    c = cfg(s1d.Scheme.Swept, u0.size, w, steps)
+    c.phys.fourier = fo
+    with s1d.Solver(c) as sv:
+        got, _, _ = sv.solve(u0)
+    return got
+
+
+def _assert_same_or_both_nan(got, want):
+    nan = np.isnan(want)
+    assert np.array_equal(np.isnan(got), nan)
+    assert_bitwise(got[~nan], want[~nan])
+
+
+@pytest.mark.parametrize("case", ["fast", "spike", "all-large", "overflow", "fo-0.5", "fo-0.6", "fo-neg"])
+@pytest.mark.parametrize("w", [64, 1024])
+def test_fast_form_guard(gpu, case, w):
+    n, steps = 1 << 16, 1500
+    x = np.arange(n)
+    u0 = np.sin(2 * np.pi * x / n) + 0.3 * np.cos(0.37 * x)
+    fo = {"fo-0.5": 0.5, "fo-0.6": 0.6, "fo-neg": -0.1}.get(case, 0.4)
+    if case == "fast":
+        u0 = u0 * 2.0 ** 1000                     # large but below 2^1022: fast form throughout
+    elif case == "spike":
+        u0[12345] = 1.6 * 2.0 ** 1022             # one CTA's inputs too large: mixed fast/exact launches
+    elif case == "all-large":
+        u0 = u0 * 2.0 ** 1021                     # every CTA falls back, no overflow anywhere
+    elif case == "overflow":
+        u0[777] = 1.5 * 2.0 ** 1023               # 2c overflows to inf in the reference
+    if case == "fo-0.6":
+        steps = 40                                # unstable: exact build only (growth stays finite here)
+    want = O.port_run_state("heat", "lengthening", u0, steps, 0.0, fourier=fo)
+    _assert_same_or_both_nan(_solve(u0, w, steps, fo), want)
