@@ -54,8 +54,9 @@ struct Shard {
     double* state[2] = {nullptr, nullptr};
     double* EL[2] = {nullptr, nullptr};
     double* ER[2] = {nullptr, nullptr};
-    unsigned* flags = nullptr; // multi-process: [0] left neighbour's rounds, [1] right's
-    int* fallback = nullptr;   // heat tiles: per-CTA verdict of the fast build (heat.cu heat_step)
+    unsigned* flags = nullptr; // multi-process: [0] left neighbour's rounds, [1] right's, [2] round base;
+                               // [8]: heat fast-form flag (heat.cu heat_step), read by the neighbours
+    int* big() const { return flags ? reinterpret_cast<int*>(flags + 8) : nullptr; }
     unsigned* cov = nullptr;   // debug runs: coverage counts [total][n]
     cudaStream_t cs = nullptr; // copy stream for pipelined host I/O (s1d_solve)
     std::vector<cudaEvent_t> ev_h2d, ev_dn; // per I/O chunk
@@ -80,13 +81,6 @@ struct ShardBlob {
 // Dead-peer guard of the device-side round waits (sticky: only the first
 // wait after a peer died pays it). 60 s by default; S1D_ROUND_TIMEOUT_S
 // overrides it (read once per process).
-// Kernel launches of one tile phase: the heat fast build is followed by its
-// gated exact build (heat.cu heat_step) when 0 <= Fo <= 0.5.
-int heat_tile_launches(bool euler, bool debug, const TileArgs& a) {
-    if (euler || debug) return 1;
-    return a.fallback && a.fourier >= 0.0 && a.fourier <= 0.5 ? 2 : 1;
-}
-
 // SM count of a device (grid sizing), cached per device.
 int device_sms(int dev) {
     static int cache[64] = {};
@@ -179,7 +173,6 @@ struct Solver {
                 cudaFree(s.ER[k]);
             }
             cudaFree(s.flags);
-            cudaFree(s.fallback);
             cudaFree(s.cov);
             cudaFree(s.err);
             cudaFree(s.staging);
@@ -264,13 +257,9 @@ struct Solver {
                 S1D_CUDA(cudaMalloc(&s.EL[k], edge_bytes));
                 S1D_CUDA(cudaMalloc(&s.ER[k], edge_bytes));
             }
-            if (!euler) // heat tile kernels: per-CTA fast/exact verdicts (one per tile bounds any grid)
-                S1D_CUDA(cudaMalloc(&s.fallback, sizeof(int) * (s.nb + 1)));
         }
-        if (mp) {
-            S1D_CUDA(cudaMalloc(&s.flags, 256));
-            S1D_CUDA(cudaMemset(s.flags, 0, 256));
-        }
+        S1D_CUDA(cudaMalloc(&s.flags, 256)); // round flags (multi-process), heat fast-form flag
+        S1D_CUDA(cudaMemset(s.flags, 0, 256));
     }
 
     void enable_peer(int d, int dn) {
@@ -709,13 +698,17 @@ struct Solver {
             a.dt_dx = cfg.dt_dx;
             a.error_flag = s.err;
             a.sms = s.sms;
-            a.fallback = s.fallback;
+            if (!euler) {
+                a.big_self = s.big();
+                a.big_left = L.big();
+                a.big_right = Rt.big();
+            }
             a.dbg = dbg_args(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             auto launch = [&](const TileArgs& ta) {
                 if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, ta, s.st, debug));
                 else S1D_CUDA(launch_heat_tile(kind, ta, s.st, debug));
-                stats.kernel_launches += heat_tile_launches(euler, debug, ta);
+                stats.kernel_launches += !euler && !debug && heat_fast_form(ta) ? 2 : 1;
             };
             if (pio && (kind == kUp || kind == kDown)) {
                 const int K = pio->K;

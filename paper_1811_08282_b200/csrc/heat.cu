@@ -66,6 +66,7 @@ __device__ __forceinline__ double heat_step(double l, double c, double r, double
 
 // |v| >= 2^1022, inf or NaN (biased exponent >= 0x7fd)
 __device__ __forceinline__ bool too_big(double v) { return (__double2hiint(v) & 0x7fffffff) >= 0x7fd00000; }
+__device__ __forceinline__ int ld_flag(const int* p) { return *reinterpret_cast<const volatile int*>(p); }
 
 __global__ void __launch_bounds__(256) heat_classic_kernel(const ClassicArgs a) {
     // Two points per thread (N is a multiple of the even block width). Only the
@@ -353,10 +354,25 @@ __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P,
 // spills; measured +4-10% over the uncapped build).
 // XS: short-tile build (m <= kXportLevels): cp.async ring init and staged
 // exports; wide tiles instantiate XS = false (code identical to before).
+// One swept phase of the CTA's G tiles. FU: the fast build (heat_step<true>),
+// followed in the same stream by the exact build gated on the shard's
+// sticky flag *a.big_self ("a value >= 2^1022 may be here"):
+//  * Up (inputs: the state): a CTA whose loaded state holds such a value
+//    sets the flag and stops before writing anything;
+//  * every CTA of a fast launch first reads its shard's and both ring
+//    neighbours' flags and, if any is set, sets its own and stops.
+// The exact build then recomputes the whole launch when the flag is set (the
+// CTAs the fast build completed had small inputs, so their exact results are
+// the same bits). Why this is enough: with 0 < Fo <= 0.5 every value of a
+// solve is a convex combination of values one launch earlier (heat_step), so
+// a launch's inputs can exceed 2^1022 only if an Up input did, and a launch
+// reads edges only from its own shard and its ring neighbours, whose flags
+// were final when their previous launch completed (the launch waits for it).
+// Without a.big_self the exact build runs ungated.
 template <int Q, int KIND, int MAXT, int MINB, int U, bool XS, bool FU>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
-    if (!FU && a.fallback && a.fallback[blockIdx.x] == 0) return; // the fast build did this CTA
+    if (!FU && a.big_self && ld_flag(a.big_self) == 0) return; // the fast build computed every CTA
     const int w = a.w, m = a.m;
     const int tt = (m + Q - 1) / Q; // slots per tile (fold_slots)
     const int nt = tt * G;
@@ -397,14 +413,14 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
 #pragma unroll
     for (int k = 0; k < Q; ++k) vl[k] = vr[k] = 0.0;
 
-    // FU (fast form, heat_step<true>): only if every input of this CTA's
-    // tiles is below 2^1022 (see heat_step; the launcher guarantees
-    // 0 <= Fo <= 0.5): the Up kernel's state, the Diamond/Down kernels'
-    // producer edges (re-read once here: a few GB/s next to the FP64-bound
-    // level loop). A CTA that finds a larger input writes nothing, records
-    // it in a.fallback, and the exact build (FU = false, gated on that
-    // record) computes its tiles in the same stream right after.
+    // FU: this shard or a ring neighbour may hold a value >= 2^1022 (flags,
+    // monotone) or an Up input is one; made uniform at the CTA's first
+    // barrier, before anything is written
+#ifdef S1D_EXP_NOFLAG
     bool big = false;
+#else
+    bool big = FU && (ld_flag(a.big_self) | ld_flag(a.big_left) | ld_flag(a.big_right)) != 0;
+#endif
     if (KIND == kUp) { // coalesced staging of the CTA's ntiles*w contiguous points
         const double* src = a.state_in + (std::size_t)bfirst * w;
         for (int j = t; j < ntiles * w; j += nt) {
@@ -413,8 +429,14 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
             if (FU) big |= too_big(v);
             stage[gg * ws + (j - gg * w)] = v;
         }
-        if (FU) big = __syncthreads_or(big);
-        else __syncthreads();
+        if (FU) {
+            if (__syncthreads_or(big)) { // nothing written yet
+                if (t == 0) atomicOr(a.big_self, 1); // sticky; propagates one shard per launch
+                return;
+            }
+        } else {
+            __syncthreads();
+        }
         const double* my = stage + g * ws; // core x-1: left d at m-1-d, right d at m+d
 #pragma unroll
         for (int k = 0; k < Q; ++k) {
@@ -463,7 +485,14 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
                 ringL[ridx(i, rmask, gg, G)] = srcL(bfirst + gg)[i];
             }
         }
-        __syncthreads();
+        if (FU) {
+            if (__syncthreads_or(big)) { // nothing written yet (XS: its copies have landed)
+                if (t == 0) atomicOr(a.big_self, 1);
+                return;
+            }
+        } else {
+            __syncthreads();
+        }
     }
     // Longer tiles: slot-0 threads queue level r+kRing-1 into the ring entries
     // freed by level r-1 (cp.async, one group per level) and wait so that
@@ -485,18 +514,6 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
 
     double* oL = a.out_L + (std::size_t)b * w;
     double* oR = a.out_R + (std::size_t)b * w;
-
-    if (FU && KIND != kUp) { // producer edges: w values per side and tile
-        for (int j = t; j < ntiles * w; j += nt) {
-            const int gg = j / w, i = j - gg * w;
-            big |= too_big(srcR(bfirst + gg)[i]) | too_big(srcL(bfirst + gg)[i]);
-        }
-        big = __syncthreads_or(big);
-    }
-    if (FU) { // this CTA's verdict for the gated exact launch that follows
-        if (t == 0) a.fallback[blockIdx.x] = big ? 1 : 0;
-        if (big) return; // nothing written yet
-    }
 
     if (KIND != kUp) {
         fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
@@ -763,6 +780,12 @@ __global__ void __launch_bounds__(256) heat_tile_debug_kernel(const TileArgs a, 
     }
 }
 
+} // namespace
+
+bool heat_fast_form(const TileArgs& a) { return a.big_self != nullptr && a.m >= 64; }
+
+namespace {
+
 int tiles_per_cta(int w, int p, int maxt = 256) {
     const int tt = fold_slots(w, p);
     int G = 1;
@@ -783,10 +806,16 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
     if (count <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((count + G - 1) / G);
-    // fast build + gated exact build when 0 <= Fo <= 0.5 (heat_step), else
-    // the exact build alone
-    const bool fast = a.fallback && a.fourier >= 0.0 && a.fourier <= 0.5;
+    // The fast build + its gated exact build for tiles of at least 64 levels
+    // (the extra launch is then noise); shorter tiles, or no flag, run the
+    // exact build alone. (0 < Fo <= 0.5, heat_step's precondition,
+    // is guaranteed by validation.)
+    const bool fast = heat_fast_form(a);
+#ifdef S1D_EXP_NOGATE
+    for (int pass = fast ? 0 : 1; pass < (fast ? 1 : 2); ++pass) {
+#else
     for (int pass = fast ? 0 : 1; pass < 2; ++pass) {
+#endif
         const bool fu = pass == 0;
         void (*k)(const TileArgs, int) =
             kind == kUp ? (fu ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, true>
@@ -800,7 +829,7 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
             if (e != cudaSuccess) return e;
         }
         TileArgs ka = a;
-        if (!fast) ka.fallback = nullptr; // ungated
+        if (!fast) ka.big_self = nullptr; // ungated exact build
         k<<<grid, nt, smem, st>>>(ka, G);
         const cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) return e;

@@ -51,7 +51,11 @@ struct TileArgs {
     int* error_flag = nullptr;      // device NonPhysicalState flag (Euler)
     double* scratch = nullptr;      // Euler tiles too wide for shared memory: per-CTA records (launcher-owned)
     int sms = 148;                  // SMs of the launching device (queried once per shard, not per launch)
-    int* fallback = nullptr;        // heat: per-CTA verdicts of the fast build (>= grid ints; null: exact only)
+    // heat fast form (heat.cu heat_step): the shard's sticky "value >= 2^1022
+    // may be present" flag and its ring neighbours' (null: exact form only)
+    int* big_self = nullptr;
+    const int* big_left = nullptr;
+    const int* big_right = nullptr;
     DebugArgs dbg;
 };
 
@@ -90,6 +94,9 @@ struct ClassicArgs {
 // `debug` selects the instrumented instantiation (coverage / perturb).
 cudaError_t launch_heat_classic(const ClassicArgs& a, cudaStream_t st);
 cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool debug = false);
+// Whether launch_heat_tile runs the fast build (+ its gated exact build, two
+// launches) for these arguments (heat.cu heat_step).
+bool heat_fast_form(const TileArgs& a);
 // Points per thread of the heat tile kernel for width w; `tiles` (the
 // smallest shard's tile count, or -1) lets small grids trade P for CTAs.
 int heat_points_per_thread(int w, long long tiles = -1);

@@ -79,7 +79,8 @@ Args parse(int argc, char** argv, int first) {
         std::string s = argv[i];
         if (s.rfind("--", 0) == 0) {
             const std::string key = s.substr(2);
-            if (i + 1 < argc && std::string(argv[i + 1]).rfind("--", 0) != 0) a.flags[key] = argv[++i];
+            const bool boolean = key == "perturb-ulp"; // takes no value
+            if (!boolean && i + 1 < argc && std::string(argv[i + 1]).rfind("--", 0) != 0) a.flags[key] = argv[++i];
             else a.flags[key] = "1";
         } else if (s.find('=') != std::string::npos) {
             const auto eq = s.find('=');
