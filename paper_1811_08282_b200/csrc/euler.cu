@@ -93,14 +93,22 @@ __device__ __forceinline__ void raise_flag(int* flag, bool bad) {
 // classic, lengthening. KIND = counter % 4 (1 PR on Q0, 2 predictor, 3 PR on
 // Q1, 0 corrector).
 // ---------------------------------------------------------------------------
+// Points per CTA pass: one pass of the CTA's threads covers the pass's
+// pressures (PR: B + 2) or interface fluxes (B + 1) exactly. (A 256-point
+// pass left one thread computing a 257th flux alone while the CTA waited at
+// the barrier: a second full div/sqrt latency chain per pass.)
+__host__ __device__ constexpr int len_classic_points(int kind) { return (kind & 1) ? kClassicB - 2 : kClassicB - 1; }
+constexpr int kFlatClassicPoints = kClassicB - 4; // B + 4 pressures per pass
+
 template <int KIND>
 __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_len_classic(const ClassicArgs a) {
+    constexpr int B = len_classic_points(KIND);
     __shared__ double sh[3][kClassicB + 2];
     const Fields F = fields_of(a);
     const double gamma = a.gamma;
     bool bad = false;
-    for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * kClassicB; i0 < a.N; i0 += (std::uint64_t)gridDim.x * kClassicB) {
-        const int nb = (int)min((std::uint64_t)kClassicB, a.N - i0);
+    for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * B; i0 < a.N; i0 += (std::uint64_t)gridDim.x * B) {
+        const int nb = (int)min((std::uint64_t)B, a.N - i0);
         const bool lb = i0 == 0, rb = i0 + nb == a.N; // boundary blocks read / feed the neighbours
         classic_round_wait(a, lb, rb);
         if (KIND & 1) {
@@ -149,6 +157,7 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_len_c
 // classic, flattening. FIN = 0 predictor (Q1 <- from Q0), 1 corrector.
 template <int FIN>
 __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_flat_classic(const ClassicArgs a) {
+    constexpr int B = kFlatClassicPoints;
     __shared__ double sp[kClassicB + 4];
     __shared__ double sf[3][kClassicB + 1];
     const Fields F = fields_of(a);
@@ -156,8 +165,8 @@ __global__ void __launch_bounds__(kClassicB, S1D_EULER_CLASSIC_MINB) euler_flat_
     const int s = FIN ? 3 : 0, ws = FIN ? 0 : 3;
     const double factor = FIN ? a.dt_dx : em::mul(0.5, a.dt_dx);
     bool bad = false;
-    for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * kClassicB; i0 < a.N; i0 += (std::uint64_t)gridDim.x * kClassicB) {
-        const int nb = (int)min((std::uint64_t)kClassicB, a.N - i0);
+    for (std::uint64_t i0 = (std::uint64_t)blockIdx.x * B; i0 < a.N; i0 += (std::uint64_t)gridDim.x * B) {
+        const int nb = (int)min((std::uint64_t)B, a.N - i0);
         const bool lb = i0 == 0, rb = i0 + nb == a.N;
         classic_round_wait(a, lb, rb);
         for (int t = threadIdx.x; t < nb + 4; t += blockDim.x) { // sp[t] = p(i0 + t - 2)
@@ -593,7 +602,7 @@ unsigned grid_for(std::uint64_t n, int per_block, int sms) {
 } // namespace
 
 cudaError_t launch_euler_classic(int flat, const ClassicArgs& a, cudaStream_t st) {
-    const unsigned grid = grid_for(a.N, kClassicB, a.sms);
+    const unsigned grid = grid_for(a.N, flat ? kFlatClassicPoints : len_classic_points((int)(a.counter & 3)), a.sms);
     if (flat) {
         if (a.counter & 1) euler_flat_classic<0><<<grid, kClassicB, 0, st>>>(a);
         else euler_flat_classic<1><<<grid, kClassicB, 0, st>>>(a);
