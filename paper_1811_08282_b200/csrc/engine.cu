@@ -249,7 +249,10 @@ struct Solver {
         S1D_CUDA(cudaMalloc(&s.state[0], state_bytes));
         S1D_CUDA(cudaMalloc(&s.state[1], state_bytes));
         S1D_CUDA(cudaMalloc(&s.err, sizeof(int)));
-        S1D_CUDA(cudaMemset(s.err, 0, sizeof(int)));
+        // Stream-ordered: the shard's stream is non-blocking, so a legacy
+        // cudaMemset (default stream) would not be ordered before its first
+        // kernel — a kernel could read the flags before they are zeroed.
+        S1D_CUDA(cudaMemsetAsync(s.err, 0, sizeof(int), s.st));
         if (euler) S1D_CUDA(cudaMalloc(&s.staging, sizeof(double) * 3 * s.N));
         if (cfg.scheme == S1D_SWEPT) {
             const std::size_t edge_bytes = sizeof(double) * s.nb * w * static_cast<std::size_t>(spec.rec);
@@ -259,7 +262,8 @@ struct Solver {
             }
         }
         S1D_CUDA(cudaMalloc(&s.flags, 256)); // round flags (multi-process), heat fast-form flag
-        S1D_CUDA(cudaMemset(s.flags, 0, 256));
+        S1D_CUDA(cudaMemsetAsync(s.flags, 0, 256, s.st));
+        S1D_CUDA(cudaStreamSynchronize(s.st)); // zeroed before any neighbour (or IPC peer) reads them
     }
 
     void enable_peer(int d, int dn) {
@@ -516,7 +520,7 @@ struct Solver {
             for (int g : locals) {
                 S1D_CUDA(cudaSetDevice(sh(g).dev));
                 S1D_CUDA(cudaMalloc(&sh(g).cov, sizeof(unsigned) * std::max<std::size_t>(cells, 1)));
-                S1D_CUDA(cudaMemset(sh(g).cov, 0, sizeof(unsigned) * std::max<std::size_t>(cells, 1)));
+                S1D_CUDA(cudaMemsetAsync(sh(g).cov, 0, sizeof(unsigned) * std::max<std::size_t>(cells, 1), sh(g).st));
             }
         }
         advance(st, tm);
@@ -1182,7 +1186,8 @@ int s1d_calibrate_transport(int dev_a, int dev_b, double* alpha, double* beta, c
             S1D_CUDA(cudaStreamCreateWithFlags(&st[i], cudaStreamNonBlocking));
             S1D_CUDA(cudaMalloc(&flag[i], 256));
             S1D_CUDA(cudaMalloc(&eflag[i], sizeof(int)));
-            S1D_CUDA(cudaMemset(eflag[i], 0, sizeof(int)));
+            S1D_CUDA(cudaMemsetAsync(eflag[i], 0, sizeof(int), st[i]));
+            S1D_CUDA(cudaStreamSynchronize(st[i]));
         }
         cudaEvent_t e0, e1;
         S1D_CUDA(cudaSetDevice(dev_a));
@@ -1192,8 +1197,8 @@ int s1d_calibrate_transport(int dev_a, int dev_b, double* alpha, double* beta, c
         auto pingpong = [&](int iters) {
             for (int i = 0; i < 2; ++i) {
                 S1D_CUDA(cudaSetDevice(devs[i]));
-                S1D_CUDA(cudaMemset(flag[i], 0, 256));
-                S1D_CUDA(cudaDeviceSynchronize());
+                S1D_CUDA(cudaMemsetAsync(flag[i], 0, 256, st[i]));
+                S1D_CUDA(cudaStreamSynchronize(st[i]));
             }
             S1D_CUDA(cudaSetDevice(dev_b));
             S1D_CUDA(s1d::launch_pingpong(flag[1], flag[0], iters, 0, eflag[1], 10000000000ull, st[1]));
@@ -1224,7 +1229,7 @@ int s1d_calibrate_transport(int dev_a, int dev_b, double* alpha, double* beta, c
         S1D_CUDA(cudaMalloc(&dst, bytes));
         S1D_CUDA(cudaSetDevice(dev_a));
         S1D_CUDA(cudaMalloc(&src, bytes));
-        S1D_CUDA(cudaMemset(src, 0, bytes));
+        S1D_CUDA(cudaMemsetAsync(src, 0, bytes, st[0]));
         S1D_CUDA(cudaMemcpyPeerAsync(dst, dev_b, src, dev_a, bytes, st[0]));
         const int reps = 4;
         S1D_CUDA(cudaEventRecord(e0, st[0]));
