@@ -46,9 +46,9 @@ CLASSIC_BYTES_PER_UPDATE = 16  # one FP64 load + one store per point-update
 
 def euler_pipe_profile():
     """FP64-pipe utilisation of the Euler swept Diamond (both methods) from the
-    committed ncu capture of this configuration (profiles/r01_euler_top_kernel.txt):
+    committed ncu capture of this configuration (profiles/r02_euler_top_kernel.txt):
     the Euler kernels are FP64-pipe bound (div/sqrt-heavy fluxes)."""
-    path = os.path.join(ROOT, "profiles", "r01_euler_top_kernel.txt")
+    path = os.path.join(ROOT, "profiles", "r02_euler_top_kernel.txt")
     out = {"bound": "fp64", "kernel": "euler_tile (swept Diamond)", "unit": "% of FP64 pipe cycles",
            "source": "ncu sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active, " + os.path.relpath(path, ROOT)}
     try:

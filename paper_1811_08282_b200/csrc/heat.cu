@@ -181,8 +181,6 @@ struct Fold {
     int sa, sb;          // slot range of my warp (warp-uniform)
     double2* F;          // [2][(tt+2)G]: (vl[0], vr[0]) of slot s at (s+1)G+g
     double2* Lst;        // [2][(tt+2)G]: (vl[Q-1], vr[Q-1]) of slot s at (s+1)G+g
-    double2* F1;         // K2 only: (vl[1], vr[1])
-    double2* Lm1;        // K2 only: (vl[Q-2], vr[Q-2])
     int xs;              // parity stride (double2 elements)
     int rmask;           // ring index mask
     int* err;            // launch error flag (checked builds: bounds violations)
@@ -201,18 +199,17 @@ __device__ __forceinline__ void level_sync() {
 #endif
 }
 
-// ph: parity of the exchange buffer (alternates with every barrier)
 template <int Q>
-__device__ __forceinline__ void fpublish(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int ph) {
-    const int i = ph * c.xs + (c.s + 1) * c.G + c.g;
+__device__ __forceinline__ void fpublish(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int r) {
+    const int i = (r & 1) * c.xs + (c.s + 1) * c.G + c.g;
     S1D_CHECK(i >= 0 && i < 2 * c.xs, c.err);
     c.F[i] = make_double2(vl[0], vr[0]);
     c.Lst[i] = make_double2(vl[Q - 1], vr[Q - 1]);
 }
 
 template <int Q, bool FU>
-__device__ __forceinline__ void fcompute(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int ph, double fo) {
-    const int par = ph * c.xs;
+__device__ __forceinline__ void fcompute(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r, double fo) {
+    const int par = (r & 1) * c.xs;
     const double2 in = c.Lst[par + c.s * c.G + c.g];      // slot s-1: distance sQ-1
     const double2 out = c.F[par + (c.s + 2) * c.G + c.g]; // slot s+1: distance sQ+Q
     S1D_CHECK(par + (c.s + 2) * c.G + c.g < 2 * c.xs, c.err);
@@ -286,10 +283,10 @@ __device__ __forceinline__ void fexpand_seg(const Fold<Q>& c, double (&vl)[Q], d
 #pragma unroll UN
     for (int r = r0; r < r1; ++r) {
         if (INS) finsert(c, vl, vr, r);
-        if (INS || CP) fpublish(c, vl, vr, r & 1);
+        if (INS || CP) fpublish(c, vl, vr, r);
         feed(r);
         level_sync();
-        if (CP) fcompute<Q, FU>(c, vl, vr, r & 1, fo);
+        if (CP) fcompute<Q, FU>(c, vl, vr, r, fo);
     }
 }
 
@@ -312,9 +309,9 @@ __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q],
     constexpr int UN = (PB && CP && !EX) ? U : 1;
 #pragma unroll UN
     for (int r = r0; r < r1; ++r) {
-        if (PB) fpublish(c, vl, vr, r & 1);
+        if (PB) fpublish(c, vl, vr, r);
         level_sync();
-        if (CP) fcompute<Q, FU>(c, vl, vr, r & 1, fo);
+        if (CP) fcompute<Q, FU>(c, vl, vr, r, fo);
         if (EX) fexport(c, vl, vr, r - c.m, oL, oR, live);
     }
 }
@@ -332,175 +329,7 @@ __device__ __forceinline__ void fcontract(const Fold<Q>& c, double (&vl)[Q], dou
     fcontract_seg<Q, U, FU, false, false, false>(c, vl, vr, e2, r1, fo, oL, oR, live);
 }
 
-// ---------------------------------------------------------------------------
-// Two levels per barrier (K2). Each slot publishes its first two and last two
-// distance pairs; after one barrier it computes level A over its distances
-// extended by one on each side (sQ-1 .. sQ+Q, from the neighbours' two
-// published pairs; for slot 0 "distance -1/-2" are the other side's 0/1) and
-// then level B over its own distances from level A. The two extra updates per
-// side are the neighbours' own values at level A, recomputed bit for bit
-// (identical arguments), so the results are those of two single levels; the
-// CTA meets half the barriers for (Q+1)/Q of the FP64 work. Expanding pairs
-// take the second level's inserts (time-rA values of distances rA, rA+1) from
-// the ring into the level-A window (POST); contracting pairs export from
-// level A and from level B. Any level left over (odd level counts) runs as a
-// single level on the same alternating exchange parity.
-// ---------------------------------------------------------------------------
-template <int Q>
-__device__ __forceinline__ void fpublish2(const Fold<Q>& c, const double (&vl)[Q], const double (&vr)[Q], int ph) {
-    const int i = ph * c.xs + (c.s + 1) * c.G + c.g;
-    S1D_CHECK(i >= 0 && i < 2 * c.xs, c.err);
-    c.F[i] = make_double2(vl[0], vr[0]);
-    c.F1[i] = make_double2(vl[1], vr[1]);
-    c.Lm1[i] = make_double2(vl[Q - 2], vr[Q - 2]);
-    c.Lst[i] = make_double2(vl[Q - 1], vr[Q - 1]);
-}
-
-template <int Q, bool FU, bool POST, bool EXP>
-__device__ __forceinline__ void fcompute2(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int ph, int rA,
-                                          double fo, double* oL, double* oR, bool live) {
-    const int par = ph * c.xs;
-    const int lo = par + c.s * c.G + c.g, hi = par + (c.s + 2) * c.G + c.g;
-    S1D_CHECK(hi < 2 * c.xs, c.err);
-    const double2 i1 = c.Lst[lo], i2 = c.Lm1[lo]; // slot s-1: distances sQ-1, sQ-2
-    const double2 o1 = c.F[hi], o2 = c.F1[hi];    // slot s+1: distances sQ+Q, sQ+Q+1
-    const bool s0 = c.s == 0;
-    // windows, index j <-> distance sQ + j - 2 (left: x-1 is d+1; right: x-1 is d-1)
-    double eL[Q + 4], eR[Q + 4];
-    eL[0] = s0 ? vr[1] : i2.x;
-    eL[1] = s0 ? vr[0] : i1.x;
-    eR[0] = s0 ? vl[1] : i2.y;
-    eR[1] = s0 ? vl[0] : i1.y;
-#pragma unroll
-    for (int k = 0; k < Q; ++k) {
-        eL[k + 2] = vl[k];
-        eR[k + 2] = vr[k];
-    }
-    eL[Q + 2] = o1.x;
-    eL[Q + 3] = o2.x;
-    eR[Q + 2] = o1.y;
-    eR[Q + 3] = o2.y;
-    double aL[Q + 3], aR[Q + 3]; // level A at j = 1 .. Q+2
-#pragma unroll
-    for (int j = 1; j <= Q + 2; ++j) {
-        aL[j] = heat_step<FU>(eL[j + 1], eL[j], eL[j - 1], fo);
-        aR[j] = heat_step<FU>(eR[j - 1], eR[j], eR[j + 1], fo);
-    }
-    if (POST) { // level rA+1's inserts: time-rA values of distances >= rA (one-sided, as finsert)
-        const int r = rA + 1, d0 = c.s * Q;
-#pragma unroll
-        for (int j = 1; j <= Q + 2; ++j) {
-            const int d = d0 + j - 2;
-            if (d >= r - 1) {
-                aL[j] = c.ringR[ridx(3 * r - 2 - d, c.rmask, c.g, c.G)];
-                aR[j] = c.ringL[ridx(r - 1 + d, c.rmask, c.g, c.G)];
-            }
-        }
-    }
-    if (EXP) {
-        double tl[Q], tr[Q];
-#pragma unroll
-        for (int k = 0; k < Q; ++k) {
-            tl[k] = aL[k + 2];
-            tr[k] = aR[k + 2];
-        }
-        fexport(c, tl, tr, rA - c.m, oL, oR, live);
-    }
-#pragma unroll
-    for (int k = 0; k < Q; ++k) {
-        vl[k] = heat_step<FU>(aL[k + 3], aL[k + 2], aL[k + 1], fo);
-        vr[k] = heat_step<FU>(aR[k + 1], aR[k + 2], aR[k + 3], fo);
-    }
-    if (EXP) fexport(c, vl, vr, rA + 1 - c.m, oL, oR, live);
-}
-
-// Expanding pairs (rA, rA+1) for rA in [p0, p1) step 2, one role per segment
-// (warp-uniform): 0 idle, 1 inserting (insert rA, POST for rA+1), 2 compute.
-template <int Q, int U, bool FU, int ROLE, class Feed>
-__device__ __forceinline__ void fexpand2_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int p0, int p1,
-                                             double fo, Feed& feed, int& ph) {
-    constexpr int UN = ROLE == 2 ? U : 1;
-#pragma unroll UN
-    for (int rA = p0; rA < p1; rA += 2) {
-        if (ROLE == 1) finsert(c, vl, vr, rA);
-        if (ROLE != 0) fpublish2(c, vl, vr, ph);
-        feed(rA);
-        feed(rA + 1);
-        level_sync();
-        if (ROLE != 0) fcompute2<Q, FU, ROLE == 1, false>(c, vl, vr, ph, rA, fo, nullptr, nullptr, false);
-        ph ^= 1;
-    }
-}
-
-// Expanding levels 1 .. 2*npairs in pairs: idle while both levels are below
-// sa*Q (no own distance is inserted or in span), inserting while rA <=
-// (sb+1)*Q (own distances take inserts at rA or their window reaches the
-// POST distances), compute-only after.
-template <int Q, int U, bool FU, class Feed>
-__device__ __forceinline__ void fexpand2(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int npairs, double fo,
-                                         Feed& feed, int& ph) {
-    const int end = 1 + 2 * npairs;
-    auto clampA = [&](int x) { // first pair start >= x, within [1, end]
-        const int v = x <= 1 ? 1 : 1 + 2 * ((x - 1 + 1) / 2);
-        return v > end ? end : v;
-    };
-    const int g1 = clampA(c.sa * Q - 1);      // first pair with rA + 1 >= sa*Q
-    const int g2 = clampA((c.sb + 1) * Q + 1); // first pair with rA > (sb+1)*Q
-    fexpand2_seg<Q, U, FU, 0>(c, vl, vr, 1, g1, fo, feed, ph);
-    fexpand2_seg<Q, U, FU, 1>(c, vl, vr, g1, g2 > g1 ? g2 : g1, fo, feed, ph);
-    fexpand2_seg<Q, U, FU, 2>(c, vl, vr, g2 > g1 ? g2 : g1, end, fo, feed, ph);
-}
-
-// Contracting pairs (rA, rA+1), rA = m+1, m+3, ...: ROLE 2 compute, 3 compute
-// with exports, 4 publish only, 0 idle.
-template <int Q, int U, bool FU, int ROLE>
-__device__ __forceinline__ void fcontract2_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int p0, int p1,
-                                               double fo, double* oL, double* oR, bool live, int& ph) {
-    constexpr int UN = ROLE == 2 ? U : 1;
-#pragma unroll UN
-    for (int rA = p0; rA < p1; rA += 2) {
-        if (ROLE != 0) fpublish2(c, vl, vr, ph);
-        level_sync();
-        if (ROLE == 2 || ROLE == 3) fcompute2<Q, FU, false, ROLE == 3>(c, vl, vr, ph, rA, fo, oL, oR, live);
-        ph ^= 1;
-    }
-}
-
-// Contracting levels m+1 .. m+2*npairs in pairs: compute while rA <=
-// 2m-1-sa*Q, exporting in pairs that reach a level >= 2m-1-(sb+1)*Q, publish
-// for one pair after the last compute pair, then idle.
-template <int Q, int U, bool FU>
-__device__ __forceinline__ void fcontract2(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int npairs, double fo,
-                                           double* oL, double* oR, bool live, int& ph) {
-    const int b = c.m + 1, end = b + 2 * npairs;
-    auto first_at = [&](int x) { // first pair start >= x, within [b, end]
-        const int v = x <= b ? b : b + 2 * ((x - b + 1) / 2);
-        return v > end ? end : v;
-    };
-    const int rce = 2 * c.m - 1 - c.sa * Q, ae = 2 * c.m - 1 - (c.sb + 1) * Q;
-    const int x0 = first_at(ae - 1);  // first pair with rA + 1 >= ae
-    const int x1 = first_at(rce + 1); // first pair with rA > rce
-    const int x2 = x1 + 2 > end ? end : x1 + 2;
-    fcontract2_seg<Q, U, FU, 2>(c, vl, vr, b, x0 < x1 ? x0 : x1, fo, oL, oR, live, ph);
-    fcontract2_seg<Q, U, FU, 3>(c, vl, vr, x0 < x1 ? x0 : x1, x1, fo, oL, oR, live, ph);
-    fcontract2_seg<Q, U, FU, 4>(c, vl, vr, x1, x2, fo, oL, oR, live, ph);
-    fcontract2_seg<Q, U, FU, 0>(c, vl, vr, x2, end, fo, oL, oR, live, ph);
-}
-
-// One contracting level with the exchange parity of the K2 schedule (odd
-// level counts), roles as in fcontract.
-template <int Q, bool FU>
-__device__ __forceinline__ void fcontract1(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r, double fo,
-                                           double* oL, double* oR, bool live, int& ph) {
-    const int rce = 2 * c.m - 1 - c.sa * Q, ae = 2 * c.m - 1 - (c.sb + 1) * Q;
-    if (r <= rce + 1) fpublish(c, vl, vr, ph);
-    level_sync();
-    if (r <= rce) fcompute<Q, FU>(c, vl, vr, ph, fo);
-    if (r >= ae && r <= rce) fexport(c, vl, vr, r - c.m, oL, oR, live);
-    ph ^= 1;
-}
-
-// Shared memory (doubles): exchange 8*(tt+2)*G (K2: 16*(tt+2)*G), then one region reused in turn:
+// Shared memory (doubles): exchange 8*(tt+2)*G, then one region reused in turn:
 // ring 4*levels*G (Diamond/Down), state staging G*(w+1) (Up/Down) and, for
 // short tiles, export staging 2*G*(w+1) (Up/Diamond, after the last ring read).
 // Slots of a folded tile: ceil(m / Q) with m = w/2 distances per side and
@@ -510,7 +339,7 @@ __device__ __forceinline__ void fcontract1(const Fold<Q>& c, double (&vl)[Q], do
 // level m, then lives in a register instead of slot tt's exchange entry.
 __host__ __device__ inline int fold_slots(int w, int P) { return (w / 2 + P / 2 - 1) / (P / 2); }
 
-__host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P, int G, bool k2 = false) {
+__host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P, int G) {
     const std::size_t tt = (std::size_t)fold_slots(w, P);
     const std::size_t ring = kind != kUp ? 4 * (std::size_t)ring_levels(w / 2) * G : 0;
     const std::size_t stage = kind != kDiamond ? (std::size_t)G * (w + 1) : 0;
@@ -518,7 +347,7 @@ __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P,
     const std::size_t xport = kind != kDown && w / 2 <= kXportLevels ? 2 * (std::size_t)G * (w + 1) : 0; // XS builds
     std::size_t region = ring > stage ? ring : stage;
     if (xport > region) region = xport;
-    return (k2 ? 16 : 8) * (tt + 2) * G + region;
+    return 8 * (tt + 2) * G + region;
 }
 
 // MINB > 1 caps registers for occupancy (P = 8: 64 registers, 4 CTAs/SM, no
@@ -540,8 +369,7 @@ __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P,
 // reads edges only from its own shard and its ring neighbours, whose flags
 // were final when their previous launch completed (the launch waits for it).
 // Without a.big_self the exact build runs ungated.
-// K2: two levels per barrier (fexpand2 / fcontract2).
-template <int Q, int KIND, int MAXT, int MINB, int U, bool XS, bool FU, bool K2>
+template <int Q, int KIND, int MAXT, int MINB, int U, bool XS, bool FU>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
     if (!FU && a.big_self && ld_flag(a.big_self) == 0) return; // the fast build computed every CTA
@@ -565,13 +393,11 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     c.xs = (tt + 2) * G;
     c.F = reinterpret_cast<double2*>(sm);
     c.Lst = c.F + 2 * c.xs;
-    c.F1 = c.Lst + 2 * c.xs; // K2 only
-    c.Lm1 = c.F1 + 2 * c.xs;
     const int rl = ring_levels(m);
     const int rmask = 2 * rl - 1;
     c.rmask = rmask;
     c.err = a.error_flag;
-    double* const region = sm + (K2 ? 16 : 8) * c.xs;
+    double* const region = sm + 8 * c.xs;
     double* const ringR = region; // [2*rl][G]
     double* const ringL = ringR + 2 * rl * G;
     double* const stage = region;        // Up/Down [G][w+1]
@@ -685,21 +511,17 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     double* oL = a.out_L + (std::size_t)b * w;
     double* oR = a.out_R + (std::size_t)b * w;
 
-    int ph = 0; // exchange parity (K2: flips with every barrier)
     if (KIND != kUp) {
-        if (K2) fexpand2<Q, U, FU>(c, vl, vr, m / 2, fo, feed, ph);
-        else fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
-        if (!K2 || (m & 1)) { // level m: full span; the halo pair (x = 0, w+1) is distance m
+        fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
+        { // level m: full span; the halo pair (x = 0, w+1) is distance m
             const int r = m;
-            if (!K2) ph = r & 1;
             finsert(c, vl, vr, r);
-            fpublish(c, vl, vr, ph);
+            fpublish(c, vl, vr, r);
             if (s == tt - 1 && m % Q == 0) // else distance m is a register of slot tt-1 (finsert)
-                c.F[ph * c.xs + (tt + 1) * G + g] =
+                c.F[(r & 1) * c.xs + (tt + 1) * G + g] =
                     make_double2(ringR[ridx(2 * (m - 1), rmask, g, G)], ringL[ridx(2 * (m - 1) + 1, rmask, g, G)]);
             level_sync();
-            fcompute<Q, FU>(c, vl, vr, ph, fo);
-            ph ^= 1;
+            fcompute<Q, FU>(c, vl, vr, r, fo);
         }
     }
     if (KIND != kDown) {
@@ -714,12 +536,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         double* eL = sx ? xL + g * ws : oL;
         double* eR = sx ? xR + g * ws : oR;
         fexport(c, vl, vr, 0, eL, eR, live);
-        if (K2) {
-            fcontract2<Q, U, FU>(c, vl, vr, (m - 1) / 2, fo, eL, eR, live, ph);
-            if ((m - 1) & 1) fcontract1<Q, FU>(c, vl, vr, 2 * m - 1, fo, eL, eR, live, ph);
-        } else {
-            fcontract<Q, U, FU>(c, vl, vr, m + 1, 2 * m, fo, eL, eR, live);
-        }
+        fcontract<Q, U, FU>(c, vl, vr, m + 1, 2 * m, fo, eL, eR, live);
         if (sx) {
             __syncthreads();
             double* gL = a.out_L + (std::size_t)bfirst * w;
@@ -973,16 +790,15 @@ int tiles_per_cta(int w, int p, int maxt = 256) {
     return G;
 }
 
-template <int P, int MAXT = 256, int MINB = 1, int U = 1, bool XS = false, bool K2 = false>
+template <int P, int MAXT = 256, int MINB = 1, int U = 1, bool XS = false>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     static_assert(P % 2 == 0, "the folded layout holds P/2 distance pairs per thread");
-    static_assert(!K2 || P >= 4, "two levels per barrier publish two pairs per side");
     if (XS != (a.m <= kXportLevels)) return cudaErrorInvalidValue;
     const int tt = fold_slots(a.w, P);
     if (tt > MAXT) return cudaErrorInvalidValue;
     const int G = tiles_per_cta(a.w, P, MAXT);
     const int nt = G * tt;
-    const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G, K2);
+    const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
     const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
     if (count <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((count + G - 1) / G);
@@ -994,12 +810,12 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     for (int pass = fast ? 0 : 1; pass < 2; ++pass) {
         const bool fu = pass == 0;
         void (*k)(const TileArgs, int) =
-            kind == kUp ? (fu ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, true, K2>
-                              : heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, false, K2>)
-            : kind == kDiamond ? (fu ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, true, K2>
-                                     : heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, false, K2>)
-                               : (fu ? heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, true, K2>
-                                     : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, false, K2>);
+            kind == kUp ? (fu ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, true>
+                              : heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, false>)
+            : kind == kDiamond ? (fu ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, true>
+                                     : heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, false>)
+                               : (fu ? heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, true>
+                                     : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, false>);
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
@@ -1080,15 +896,6 @@ cudaError_t launch_tile_debug(int kind, const TileArgs& a, cudaStream_t st) {
     return cudaGetLastError();
 }
 
-// Two levels per barrier for the wide P = 16 tiles (S1D_HEAT_K2=0/1, read once).
-bool heat_k2() {
-    static const bool on = [] {
-        const char* e = std::getenv("S1D_HEAT_K2");
-        return e && e[0] == '1';
-    }();
-    return on;
-}
-
 cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool debug) {
     if (debug) {
         // the instrumented kernel's contiguous layout needs P | w, w/P <= 256
@@ -1118,7 +925,6 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     case 16: // measured (n = 2^27): 4 CTAs/SM + unroll 2 from w = 256 (1.95-1.97 T), 3 CTAs/SM at w = 128
         if (xs) return launch_tile_p<16, 256, 1, 1, true>(kind, a, st);
         if (a.w < 256) return launch_tile_p<16, 256, 3, 1>(kind, a, st);
-        if (heat_k2()) return launch_tile_p<16, 256, 4, 2, false, true>(kind, a, st);
         return launch_tile_p<16, 256, 4, 2>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
