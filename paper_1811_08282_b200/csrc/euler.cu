@@ -256,12 +256,15 @@ inline int euler_tiles_per_cta(int flat, int w) {
 // bound, R/core/src/swept.cpp:10-19) keep records, pressures and fluxes in a
 // per-CTA global scratch block (L1/L2-resident) and only the edge ring in
 // shared memory; same code, same barriers, same arithmetic.
-template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false>
+// WT > 0: the tile width (and then the CTA size, MAXT) as compile-time
+// constants, so tile offsets fold into immediates (the common widths).
+template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false, int WT = 0>
 __global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1 : S1D_EULER_MINB) euler_tile(const TileArgs a, int GT) {
     using G = TileGeom<FLAT>;
     constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
     extern __shared__ double sm[];
-    const int w = a.w, m = a.m, t = threadIdx.x, NT = blockDim.x;
+    const int w = WT ? WT : a.w, m = WT ? WT / (2 * H) : a.m, t = threadIdx.x;
+    const int NT = WT ? MAXT : (int)blockDim.x;
     const int W2 = w + 2 * H;
     const std::size_t TR = (std::size_t)REC * W2 + 4 * (std::size_t)(W2 + 1); // records + pressures + fluxes
     const std::size_t TRING = 2 * (std::size_t)kERing * LVL;
@@ -529,15 +532,15 @@ std::size_t smem_optin() {
     return v;
 }
 
-template <int FLAT, bool DBG = false, int MAXT = 256, bool GMEM = false>
+template <int FLAT, bool DBG = false, int MAXT = 256, bool GMEM = false, int WT = 0>
 cudaError_t launch_tile_f(int kind, const TileArgs& a_in, cudaStream_t st, int cap_threads = 0) {
     TileArgs a = a_in;
     const int GT = GMEM ? 1 : euler_tiles_per_cta(FLAT, a.w);
     const std::size_t ring_doubles = 2 * (std::size_t)kERing * TileGeom<FLAT>::LVL;
     const size_t smem = GMEM ? GT * ring_doubles * sizeof(double) : (size_t)GT * euler_tile_smem(FLAT, a.w);
-    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, GMEM>
-                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, GMEM>
-                                                        : euler_tile<FLAT, kDown, DBG, MAXT, GMEM>;
+    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, GMEM, WT>
+                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, GMEM, WT>
+                                                        : euler_tile<FLAT, kDown, DBG, MAXT, GMEM, WT>;
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -550,6 +553,7 @@ cudaError_t launch_tile_f(int kind, const TileArgs& a_in, cudaStream_t st, int c
     if (nt > cap) nt = cap;
     const int need = 32 * ((2 * TileGeom<FLAT>::CHUNKS * GT + 31) / 32); // feeder threads
     if (nt < need) nt = need;
+    if (WT && (a.w != WT || nt != MAXT)) return cudaErrorInvalidValue; // compile-time shape must match
     const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
     if (count <= 0) return cudaSuccess;
     const unsigned grid = (unsigned)((count + GT - 1) / GT);
@@ -638,6 +642,11 @@ cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_
     if (const char* e = std::getenv("S1D_EULER_NT")) wide = std::atoi(e) > 256;
     if (wide || cap)
         return flat ? launch_tile_f<1, false, 1024>(kind, a, st, cap) : launch_tile_f<0, false, 1024>(kind, a, st, cap);
+#ifdef S1D_EULER_WT
+    if (a.w == 512 && euler_tiles_per_cta(flat, a.w) == 1)
+        return flat ? launch_tile_f<1, false, 256, false, 512>(kind, a, st)
+                    : launch_tile_f<0, false, 256, false, 512>(kind, a, st);
+#endif
     return flat ? launch_tile_f<1>(kind, a, st) : launch_tile_f<0>(kind, a, st);
 }
 
