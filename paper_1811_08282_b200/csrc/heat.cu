@@ -834,7 +834,7 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
 int heat_points_per_thread(int w, long long tiles) {
     if (const char* e = std::getenv("S1D_HEAT_P")) {
         const int p = std::atoi(e);
-        if ((p == 2 || p == 4 || p == 8 || p == 16 || p == 32) && fold_slots(w, p) <= 256) return p;
+        if ((p == 2 || p == 4 || p == 8 || p == 16) && fold_slots(w, p) <= 256) return p;
     }
     // Folded layout: P even (P/2 distance pairs per thread), ceil(m / (P/2))
     // slots (fold_slots: a ragged last slot pads). Measured on B200 (n = 2^27,
@@ -926,11 +926,6 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
         if (xs) return launch_tile_p<16, 256, 1, 1, true>(kind, a, st);
         if (a.w < 256) return launch_tile_p<16, 256, 3, 1>(kind, a, st);
         return launch_tile_p<16, 256, 4, 2>(kind, a, st);
-#ifdef S1D_HEAT_P32
-    case 32: // experiment: twice the work per barrier at 2 CTAs/SM
-        if (xs || a.w < 512) return cudaErrorInvalidValue;
-        return launch_tile_p<32, 256, 2, 1>(kind, a, st);
-#endif
     default: return cudaErrorInvalidValue;
     }
 }
