@@ -782,6 +782,8 @@ bool heat_fast_form(const TileArgs& a) { return a.big_self != nullptr && a.m >= 
 
 namespace {
 
+constexpr int kWideCta = 512; // threads per CTA of the P = 16 tiles from w = 256
+
 int tiles_per_cta(int w, int p, int maxt = 256) {
     const int tt = fold_slots(w, p);
     int G = 1;
@@ -862,8 +864,10 @@ int heat_points_per_thread(int w, long long tiles) {
                 sms = 148;
             }
         }
-        const long long g = tiles_per_cta(w, 16);
-        if ((tiles + g - 1) / g < 4LL * sms) p = 8;
+        // P = 16 runs 2 CTAs of kWideCta threads per SM from w = 256, 3 CTAs
+        // of 256 below (launch_heat_tile)
+        const long long g = w >= 256 ? tiles_per_cta(w, 16, kWideCta) : tiles_per_cta(w, 16);
+        if ((tiles + g - 1) / g < (w >= 256 ? 2LL : 4LL) * sms) p = 8;
     }
     return p;
 }
@@ -925,7 +929,12 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     case 16: // measured (n = 2^27): 4 CTAs/SM + unroll 2 from w = 256 (1.95-1.97 T), 3 CTAs/SM at w = 128
         if (xs) return launch_tile_p<16, 256, 1, 1, true>(kind, a, st);
         if (a.w < 256) return launch_tile_p<16, 256, 3, 1>(kind, a, st);
-        return launch_tile_p<16, 256, 4, 2>(kind, a, st);
+        // 512-thread CTAs (2 per SM, 64 registers): twice the tiles per CTA, so
+        // a warp spans half the distances and the busy/idle boundary of each
+        // level wastes half as many lanes. Measured (n = 2^27) against 256-thread
+        // CTAs at 4 per SM: w = 256 / 1024 / 2048: 2.27 / 2.17 / 2.14 T vs
+        // 2.13 / 2.10 / 2.09 T; 1024-thread CTAs: 1.99 / 2.09 T.
+        return launch_tile_p<16, kWideCta, 2, 2>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
 }
