@@ -126,6 +126,7 @@ struct Solver {
     bool euler = false, flat = false;
     double setup_seconds = 0.0;
     bool debug = false, perturb = false; // instrumented kernels (s1d_run_debug)
+    bool heat_exact_only = false;        // single process: the fast form's flags tripped (heat.cu heat_step)
     // Pipelined host I/O (s1d_solve): H2D of chunk k overlaps the UpTriangle
     // of chunk k-1, D2H of chunk k overlaps the DownTriangle of chunk k+1.
     struct PipeIO {
@@ -395,10 +396,12 @@ struct Solver {
     // inc/kernels.hpp:144-149). local_slice: `host` holds only the local
     // shard's points (multi-process), else the global array.
     void upload(const double* host, bool local_slice) {
+        if (!mp) heat_exact_only = false;
         for (int g : locals) {
             Shard& s = sh(g);
             const double* src = host + (local_slice ? 0 : s.start * spec.vpp);
             S1D_CUDA(cudaSetDevice(s.dev));
+            if (!mp && s.flags) S1D_CUDA(cudaMemsetAsync(s.big(), 0, sizeof(int), s.st)); // new data: re-arm
             if (!euler) {
                 S1D_CUDA(cudaMemcpyAsync(s.ic, src, sizeof(double) * s.N, cudaMemcpyHostToDevice, s.st));
             } else {
@@ -702,17 +705,21 @@ struct Solver {
             a.dt_dx = cfg.dt_dx;
             a.error_flag = s.err;
             a.sms = s.sms;
-            if (!euler) {
+            if (!euler && !heat_exact_only) {
                 a.big_self = s.big();
                 a.big_left = L.big();
                 a.big_right = Rt.big();
+                // single process: no gated launch per phase; advance() reads the
+                // flags after the run (one process per GPU cannot: every rank
+                // would have to agree to rerun)
+                a.gated = mp ? 1 : 0;
             }
             a.dbg = dbg_args(g);
             S1D_CUDA(cudaSetDevice(s.dev));
             auto launch = [&](const TileArgs& ta) {
                 if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, ta, s.st, debug));
                 else S1D_CUDA(launch_heat_tile(kind, ta, s.st, debug));
-                stats.kernel_launches += !euler && !debug && heat_fast_form(ta) ? 2 : 1;
+                stats.kernel_launches += !euler && !debug && heat_fast_form(ta) && ta.gated ? 2 : 1;
             };
             if (pio && (kind == kUp || kind == kDown)) {
                 const int K = pio->K;
@@ -846,6 +853,23 @@ struct Solver {
             s.final_state = cur[static_cast<std::size_t>(g)];
         }
         S1D_CUDA(cudaGetLastError());
+        if (!mp && !euler && !heat_exact_only && cfg.scheme == S1D_SWEPT && !debug) {
+            // heat fast form, single process: a set flag means some fast CTA
+            // stopped (an input >= 2^1022, heat.cu heat_step); rerun the whole
+            // advance in the exact form (the initial state in ic is intact)
+            int big = 0;
+            for (int g : locals) {
+                int b = 0;
+                S1D_CUDA(cudaSetDevice(sh(g).dev));
+                S1D_CUDA(cudaMemcpy(&b, sh(g).big(), sizeof(int), cudaMemcpyDeviceToHost));
+                big |= b;
+            }
+            if (big) {
+                heat_exact_only = true;
+                advance(stats_out, timing_out);
+                return;
+            }
+        }
         if (flag & 4) throw Error(S1D_INTERNAL, "device bounds check failed (checked build)");
         if (flag & 2) throw Error(S1D_TRANSPORT_ABORTED, "a neighbour shard stopped responding (round timeout)");
         if (flag) throw Error(S1D_NONPHYSICAL, "non-physical state encountered on the device");
@@ -912,6 +936,7 @@ struct Solver {
             tm->d2h_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t2).count();
             return;
         }
+        if (!mp) heat_exact_only = false; // new data (flags re-armed by the uploads below)
         PipeIO io;
         io.in = host_in;
         io.out = host_out;
@@ -923,6 +948,7 @@ struct Solver {
         for (int g : locals) {
             Shard& s = sh(g);
             ensure_pipe(s, io.K);
+            if (!mp && s.flags) S1D_CUDA(cudaMemsetAsync(s.big(), 0, sizeof(int), s.st)); // new data: re-arm
             const std::uint64_t wu = cfg.block_width;
             const double* src = host_in + (io.local ? 0 : s.start * spec.vpp);
             for (int k = 0; k < io.K; ++k) {

@@ -806,10 +806,11 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     const unsigned grid = (unsigned)((count + G - 1) / G);
     // The fast build + its gated exact build for tiles of at least 64 levels
     // (the extra launch is then noise); shorter tiles, or no flag, run the
-    // exact build alone. (0 < Fo <= 0.5, heat_step's precondition,
+    // exact build alone. With a.gated == 0 (single process) the engine reads
+    // the flags after the run instead and reruns it exactly if one is set. (0 < Fo <= 0.5, heat_step's precondition,
     // is guaranteed by validation.)
     const bool fast = heat_fast_form(a);
-    for (int pass = fast ? 0 : 1; pass < 2; ++pass) {
+    for (int pass = fast ? 0 : 1; pass < (fast && !a.gated ? 1 : 2); ++pass) {
         const bool fu = pass == 0;
         void (*k)(const TileArgs, int) =
             kind == kUp ? (fu ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, true>

@@ -56,6 +56,7 @@ struct TileArgs {
     int* big_self = nullptr;
     const int* big_left = nullptr;
     const int* big_right = nullptr;
+    int gated = 1; // 1: the gated exact build follows each fast launch; 0: the host checks the flags after the run
     DebugArgs dbg;
 };
 

@@ -66,6 +66,30 @@ def main():
             failures += not ok
             print(f"{'ok ' if ok else 'BAD'} {eq}/{me}/{sc} n={n} w={w} wf={wf} T={T} ranks={world} "
                   f"rounds={parts[0][3]} loop={tm.loop_seconds * 1e3:.2f} ms", flush=True)
+    # heat fast form's guard across processes (heat.cu heat_step): a spike
+    # >= 2^1022 near rank 0's right seam flags rank 0's Up; the flag spreads
+    # to the neighbours' launches through the IPC-shared flag words, the gated
+    # exact builds recompute, and the result is the oracle's, bit for bit
+    n, w, T = 96 * 256, 256, 700
+    cfg = s1d.LaunchConfig(equation=s1d.Equation.Heat, scheme=s1d.Scheme.Swept, grid_size=n, block_width=w,
+                           ranks=world, steps=T)
+    x = np.arange(n)
+    u0 = np.sin(2 * np.pi * x / n) + 0.3 * np.cos(0.37 * x)
+    u0[n // world - 5] = 1.6 * 2.0 ** 1022
+    with open_ring_shard(cfg) as shard:
+        out, _, _ = shard.solve(u0[shard.start:shard.start + shard.count])
+        parts = [None] * world
+        dist.all_gather_object(parts, (shard.start, out))
+    if rank == 0:
+        from oracle import oracle as O
+        glob = np.empty(n)
+        for start, arr in parts:
+            glob[start:start + arr.size] = arr
+        want = O.port_run_state("heat", "lengthening", u0, T, 0.0)
+        ok = np.array_equal(glob.view(np.uint64), want.view(np.uint64))
+        failures += not ok
+        print(f"{'ok ' if ok else 'BAD'} heat fast-form guard, spike >= 2^1022, n={n} w={w} T={T} ranks={world}",
+              flush=True)
     dist.barrier()
     code = [failures]
     dist.broadcast_object_list(code, src=0)
