@@ -242,7 +242,7 @@ typedef struct s1d_record {
     double avg_us_per_step;
     double setup_us;
     uint64_t messages_sent, bytes_sent, exchange_rounds;
-    double virtual_comm_us; /* always 0 on the B200 path */
+    double virtual_comm_us; /* CommStats::virtual_comm_time in microseconds (the alpha-beta model) */
 } s1d_record;
 /* measure (src/perf.cpp:29-32): one run of cfg, reduced to a record. */
 int s1d_measure(const s1d_config* cfg, s1d_record* out, char* err, size_t errlen);
