@@ -17,6 +17,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <memory>
 #include <string>
 #include <vector>
@@ -61,6 +62,9 @@ struct Shard {
     cudaStream_t cs = nullptr; // copy stream for pipelined host I/O (s1d_solve)
     std::vector<cudaEvent_t> ev_h2d, ev_dn; // per I/O chunk
     cudaEvent_t ev_fin = nullptr;           // final-slice D2H ordering
+    cudaStream_t st2 = nullptr;             // second compute stream of the wavefront solve
+    std::vector<cudaEvent_t> ev_chunk;      // wavefront solve: [phase slot][chunk] completion
+    cudaEvent_t ev_mid = nullptr, ev_join = nullptr;
     int* err = nullptr;
     double* staging = nullptr; // AoS (vpp = 3) upload/download buffer (Euler)
     const double* final_state = nullptr;
@@ -134,6 +138,7 @@ struct Solver {
         double* out = nullptr;
         bool local = false;
         int K = 1;
+        bool wave = false; // wavefront schedule (wavefront())
     };
     PipeIO* pio = nullptr;
     std::string last_error;
@@ -185,6 +190,10 @@ struct Solver {
             for (cudaEvent_t e : s.ev_h2d) cudaEventDestroy(e);
             for (cudaEvent_t e : s.ev_dn) cudaEventDestroy(e);
             if (s.ev_fin) cudaEventDestroy(s.ev_fin);
+            for (cudaEvent_t e : s.ev_chunk) cudaEventDestroy(e);
+            if (s.ev_mid) cudaEventDestroy(s.ev_mid);
+            if (s.ev_join) cudaEventDestroy(s.ev_join);
+            if (s.st2) cudaStreamDestroy(s.st2);
             if (s.cs) cudaStreamDestroy(s.cs);
             if (s.st) cudaStreamDestroy(s.st);
         }
@@ -473,10 +482,20 @@ struct Solver {
                 static_cast<int>((static_cast<long long>(nb) * (k + 1)) / K)};
     }
 
-    void ensure_pipe(Shard& s, int K) {
+    void ensure_pipe(Shard& s, int K, bool wave) {
         S1D_CUDA(cudaSetDevice(s.dev));
         if (!s.cs) S1D_CUDA(cudaStreamCreateWithFlags(&s.cs, cudaStreamNonBlocking));
         if (!s.ev_fin) S1D_CUDA(cudaEventCreateWithFlags(&s.ev_fin, cudaEventDisableTiming));
+        if (wave) {
+            if (!s.st2) S1D_CUDA(cudaStreamCreateWithFlags(&s.st2, cudaStreamNonBlocking));
+            if (!s.ev_mid) S1D_CUDA(cudaEventCreateWithFlags(&s.ev_mid, cudaEventDisableTiming));
+            if (!s.ev_join) S1D_CUDA(cudaEventCreateWithFlags(&s.ev_join, cudaEventDisableTiming));
+            while (static_cast<int>(s.ev_chunk.size()) < wave_slots * K) {
+                cudaEvent_t e;
+                S1D_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+                s.ev_chunk.push_back(e);
+            }
+        }
         while (static_cast<int>(s.ev_h2d.size()) < K) {
             cudaEvent_t a, b;
             S1D_CUDA(cudaEventCreateWithFlags(&a, cudaEventDisableTiming));
@@ -486,15 +505,17 @@ struct Solver {
         }
     }
 
-    // D2H (Euler: pack first) of shard positions [p0, p1) once `after` is done.
-    void chunk_d2h(Shard& s, std::uint64_t p0, std::uint64_t p1, cudaEvent_t after) {
+    // D2H (Euler: pack first, on `stream`) of shard positions [p0, p1) once
+    // `after` is done (heat: recorded by the caller).
+    void chunk_d2h(Shard& s, std::uint64_t p0, std::uint64_t p1, cudaEvent_t after, cudaStream_t stream = nullptr) {
+        if (!stream) stream = s.st;
         double* dst = pio->out + (pio->local ? 0 : s.start * spec.vpp) + p0 * spec.vpp;
         if (!euler) {
             S1D_CUDA(cudaStreamWaitEvent(s.cs, after, 0));
             S1D_CUDA(cudaMemcpyAsync(dst, s.state[0] + p0, sizeof(double) * (p1 - p0), cudaMemcpyDeviceToHost, s.cs));
         } else {
-            S1D_CUDA(launch_euler_pack(s.state[0] + p0, s.staging + 3 * p0, p1 - p0, s.fstride, s.st));
-            S1D_CUDA(cudaEventRecord(after, s.st));
+            S1D_CUDA(launch_euler_pack(s.state[0] + p0, s.staging + 3 * p0, p1 - p0, s.fstride, stream));
+            S1D_CUDA(cudaEventRecord(after, stream));
             S1D_CUDA(cudaStreamWaitEvent(s.cs, after, 0));
             S1D_CUDA(cudaMemcpyAsync(dst, s.staging + 3 * p0, sizeof(double) * 3 * (p1 - p0), cudaMemcpyDeviceToHost,
                                      s.cs));
@@ -670,12 +691,11 @@ struct Solver {
         }
     }
 
-    void swept_phase(int kind, std::int64_t j, s1d_stats& stats, bool dom_first = false, bool dom_last = false) {
-        wait_neighbours();
-        if (dom_first) record_all(&Shard::ev_dom0);
+    // Launch arguments of swept phase j (0: Up, cycles: Down) on shard g.
+    TileArgs phase_args(int kind, std::int64_t j, int g) {
         const int w = static_cast<int>(cfg.block_width);
         const int src = static_cast<int>((j + 1) & 1), dst = static_cast<int>(j & 1);
-        for (int g : locals) {
+        {
             Shard& s = sh(g);
             Shard& L = left_of(g);
             Shard& Rt = right_of(g);
@@ -715,12 +735,25 @@ struct Solver {
                 a.gated = mp ? 1 : 0;
             }
             a.dbg = dbg_args(g);
+            return a;
+        }
+    }
+
+    void launch_tiles(int kind, const TileArgs& ta, cudaStream_t stream, s1d_stats& stats) {
+        if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, ta, stream, debug));
+        else S1D_CUDA(launch_heat_tile(kind, ta, stream, debug));
+        stats.kernel_launches += !euler && !debug && heat_fast_form(ta) && ta.gated ? 2 : 1;
+    }
+
+    void swept_phase(int kind, std::int64_t j, s1d_stats& stats, bool dom_first = false, bool dom_last = false) {
+        wait_neighbours();
+        if (dom_first) record_all(&Shard::ev_dom0);
+        const int w = static_cast<int>(cfg.block_width);
+        for (int g : locals) {
+            Shard& s = sh(g);
+            const TileArgs a = phase_args(kind, j, g);
             S1D_CUDA(cudaSetDevice(s.dev));
-            auto launch = [&](const TileArgs& ta) {
-                if (euler) S1D_CUDA(launch_euler_tile(flat ? 1 : 0, kind, ta, s.st, debug));
-                else S1D_CUDA(launch_heat_tile(kind, ta, s.st, debug));
-                stats.kernel_launches += !euler && !debug && heat_fast_form(ta) && ta.gated ? 2 : 1;
-            };
+            auto launch = [&](const TileArgs& ta) { launch_tiles(kind, ta, s.st, stats); };
             if (pio && (kind == kUp || kind == kDown)) {
                 const int K = pio->K;
                 const std::uint64_t wu = static_cast<std::uint64_t>(w);
@@ -755,6 +788,146 @@ struct Solver {
         }
         if (dom_last) record_all(&Shard::ev_dom1);
         record_round();
+    }
+
+    // Wavefront solve (s1d_solve, one shard in this process, aligned swept
+    // run): the host copies take ~10% of a 2^27-point solve (1 GiB each way
+    // over PCIe), more than the Up and Down phases they used to hide behind.
+    // The first wave_head Diamonds after the Up and the last wave_tail before
+    // the Down therefore also run per chunk of tiles, on two streams, each
+    // chunk after its neighbour chunks of the previous phase (tile b reads
+    // the edges of tiles b-1..b+1 and its outputs overwrite the buffers those
+    // tiles' readers use, so the three-chunk dependency covers both RAW and
+    // WAR): the copy-in of chunk k overlaps the first phases of the chunks
+    // before it, and the copy-out of chunk k the last phases of the chunks
+    // after it. The ring wraps (chunk 0's left neighbour is chunk K-1), so
+    // the head wave grows from chunk 0 upwards and finishes the low chunks
+    // last. Multi-shard runs keep the Up/Down-only pipeline.
+    // Shape: 16 chunks and enough pipelined Diamonds that their compute
+    // covers one copy of the state. A heat Diamond takes ~m/340 of the copy
+    // time (m updates per point at ~2.3 T/s against 8 B per point over PCIe
+    // at ~55 GB/s), so ceil(256/m) Diamonds plus the Up: 2 at the bench's
+    // m = 128 (the best of 1..6 measured there: 370 ms against 390 ms for the
+    // Up/Down-only pipeline). Where one Diamond would do (heat m >= 256, and
+    // Euler, whose updates cost ~100x more) the Up and Down already hide most
+    // of the copies and the chunked Diamonds cost more than they save
+    // (measured: even at m = 512, 4% slower for Euler at w = 512), so those
+    // keep the Up/Down-only pipeline. S1D_WAVE = "chunks,head,tail" forces a
+    // shape (development knob). Returns whether to use the wavefront.
+    int wave_head = 0, wave_tail = 0, wave_slots = 0, wave_chunks = 16;
+    bool set_wave_shape() {
+        const int mm = static_cast<int>(m);
+        wave_head = euler ? 1 : std::min(6, std::max(1, (256 + mm - 1) / mm));
+        wave_tail = wave_head;
+        wave_chunks = 16;
+        bool use = wave_head >= 2;
+        if (const char* e = std::getenv("S1D_WAVE")) {
+            int k = 0, h = 0, t = 0;
+            if (std::sscanf(e, "%d,%d,%d", &k, &h, &t) == 3 && k >= 3 && h >= 0 && t >= 0) {
+                wave_chunks = k;
+                wave_head = h;
+                wave_tail = t;
+                use = true;
+            }
+        }
+        wave_slots = wave_head + 1 + wave_tail + 1; // Up, head Diamonds, tail Diamonds, Down
+        return use;
+    }
+    std::int64_t dom_diamonds = 0; // Diamonds inside the dominant-kernel timing window
+
+    bool wavefront(std::int64_t cycles) const {
+        return pio && pio->wave && !mp && R() == 1 && locals.size() == 1 && !debug &&
+               cycles >= wave_head + wave_tail + 2 && pio->K >= 3;
+    }
+
+    // Chunk c of swept phase p (0: Up, cycles: Down) on `stream`.
+    void chunk_phase(std::int64_t p, std::int64_t cycles, int c, cudaStream_t stream, s1d_stats& stats) {
+        const int g = locals[0];
+        Shard& s = sh(g);
+        const int kind = p == 0 ? kUp : (p == cycles ? kDown : kDiamond);
+        TileArgs ta = phase_args(kind, p, g);
+        const auto [t0, t1] = chunk_tiles(s, c, pio->K);
+        ta.b0 = t0;
+        ta.b1 = t1;
+        const std::uint64_t wu = cfg.block_width;
+        if (kind == kUp) {
+            S1D_CUDA(cudaStreamWaitEvent(stream, s.ev_h2d[static_cast<std::size_t>(c)], 0));
+            if (euler)
+                S1D_CUDA(launch_euler_unpack(s.staging + 3 * t0 * wu, s.ic + t0 * wu, (t1 - t0) * wu, s.fstride,
+                                             spec.rec, stream));
+        }
+        launch_tiles(kind, ta, stream, stats);
+        if (kind == kDown) { // as in swept_phase
+            cudaEvent_t e = s.ev_dn[static_cast<std::size_t>(c)];
+            S1D_CUDA(cudaEventRecord(e, stream));
+            const std::uint64_t p0 = ta.seam ? t0 * wu + wu / 2 : t0 * wu;
+            const std::uint64_t p1 = std::min<std::uint64_t>(ta.seam ? t1 * wu + wu / 2 : t1 * wu, s.N);
+            if (p1 > p0) chunk_d2h(s, p0, p1, e, stream);
+        }
+    }
+
+    void wavefront_phases(std::int64_t cycles, s1d_stats& stats) {
+        Shard& s = sh(locals[0]);
+        S1D_CUDA(cudaSetDevice(s.dev));
+        const int K = pio->K;
+        const std::int64_t tail0 = cycles - wave_tail; // first tail phase
+        const cudaStream_t sts[2] = {s.st, s.st2};
+        auto slot = [&](std::int64_t p) {
+            return p <= wave_head ? static_cast<int>(p) : wave_head + 1 + static_cast<int>(p - tail0);
+        };
+        auto wrap = [&](int c) { return ((c % K) + K) % K; };
+        std::vector<char> done(static_cast<std::size_t>(wave_slots * K), 0);
+        auto is_done = [&](std::int64_t p, int c) -> char& {
+            return done[static_cast<std::size_t>(slot(p) * K + wrap(c))];
+        };
+        auto ev = [&](std::int64_t p, int c) { return s.ev_chunk[static_cast<std::size_t>(slot(p) * K + wrap(c))]; };
+        auto issue = [&](std::int64_t p, int c) {
+            const cudaStream_t stream = sts[c & 1];
+            if (p == tail0) {
+                S1D_CUDA(cudaStreamWaitEvent(stream, s.ev_mid, 0));
+            } else if (p > 0) {
+                for (int d = -1; d <= 1; ++d) S1D_CUDA(cudaStreamWaitEvent(stream, ev(p - 1, c + d), 0));
+            }
+            chunk_phase(p, cycles, c, stream, stats);
+            S1D_CUDA(cudaEventRecord(ev(p, c), stream));
+            is_done(p, c) = 1;
+        };
+        S1D_CUDA(cudaStreamWaitEvent(s.st2, s.ev_start, 0));
+        // head: Up chunk a once its copy is queued; every head Diamond chunk as
+        // soon as its three neighbours of the previous phase are issued
+        auto drain = [&] {
+            for (bool progress = true; progress;) {
+                progress = false;
+                for (std::int64_t p = 1; p <= wave_head; ++p)
+                    for (int c = 0; c < K; ++c)
+                        if (!is_done(p, c) && is_done(p - 1, c - 1) && is_done(p - 1, c) && is_done(p - 1, c + 1)) {
+                            issue(p, c);
+                            progress = true;
+                        }
+            }
+        };
+        for (int a = 0; a < K; ++a) {
+            drain();
+            issue(0, a);
+        }
+        drain();
+        // middle: whole-shard Diamonds on s.st after every head chunk
+        for (int c = 0; c < K; ++c) S1D_CUDA(cudaStreamWaitEvent(s.st, ev(wave_head, c), 0));
+        record_all(&Shard::ev_dom0);
+        for (std::int64_t j = wave_head + 1; j < tail0; ++j) swept_phase(kDiamond, j, stats);
+        record_all(&Shard::ev_dom1);
+        dom_diamonds = tail0 - wave_head - 1;
+        S1D_CUDA(cudaEventRecord(s.ev_mid, s.st));
+        // tail: Down chunks in order 0..K-1, each after the cone of tail
+        // chunks it needs (depth-first), so the copy-out starts early
+        std::function<void(std::int64_t, int)> need = [&](std::int64_t p, int c) {
+            if (p < tail0 || is_done(p, c)) return;
+            for (int d = -1; d <= 1; ++d) need(p - 1, c + d);
+            issue(p, wrap(c));
+        };
+        for (int c = 0; c < K; ++c) need(cycles, c);
+        S1D_CUDA(cudaEventRecord(s.ev_join, s.st2));
+        S1D_CUDA(cudaStreamWaitEvent(s.st, s.ev_join, 0));
     }
 
     void advance(s1d_stats* stats_out, s1d_timing* timing_out) {
@@ -793,7 +966,12 @@ struct Solver {
         const bool dom_diamond = cycles >= 2;
         const bool dom_classic = !dom_diamond && pad > 0;
         const bool dom_updown = !dom_diamond && !dom_classic && cycles == 1;
-        if (cycles >= 1) {
+        dom_diamonds = cycles - 1;
+        if (cycles >= 1 && wavefront(cycles)) {
+            wavefront_phases(cycles, stats);
+            cur_idx = 0;
+            for (int g = 0; g < R(); ++g) cur[static_cast<std::size_t>(g)] = sh(g).state[0];
+        } else if (cycles >= 1) {
             swept_phase(kUp, 0, stats, dom_updown, false);
             for (std::int64_t j = 1; j <= cycles; ++j)
                 swept_phase(j == cycles ? kDown : kDiamond, j, stats, dom_diamond && j == 1,
@@ -902,8 +1080,8 @@ struct Solver {
             for (int g : locals) pts += sh(g).N;
             const char* name = "";
             if (dom_diamond) {
-                timing_out->dominant_launches = static_cast<std::uint64_t>(cycles - 1);
-                timing_out->dominant_point_updates = static_cast<std::uint64_t>(cycles - 1) * m * pts;
+                timing_out->dominant_launches = static_cast<std::uint64_t>(dom_diamonds);
+                timing_out->dominant_point_updates = static_cast<std::uint64_t>(dom_diamonds) * m * pts;
                 name = "swept_diamond";
             } else if (dom_classic) {
                 timing_out->dominant_launches = static_cast<std::uint64_t>(pad);
@@ -943,11 +1121,12 @@ struct Solver {
         io.local = local_io();
         std::uint64_t min_nb = ~0ull;
         for (int g : locals) min_nb = std::min<std::uint64_t>(min_nb, sh(g).nb);
-        io.K = static_cast<int>(std::min<std::uint64_t>(8, min_nb));
+        io.wave = set_wave_shape() && !mp && R() == 1 && locals.size() == 1 && cycles >= wave_head + wave_tail + 2 && min_nb >= 3;
+        io.K = static_cast<int>(std::min<std::uint64_t>(io.wave ? wave_chunks : 8, min_nb));
         sync_all();
         for (int g : locals) {
             Shard& s = sh(g);
-            ensure_pipe(s, io.K);
+            ensure_pipe(s, io.K, io.wave);
             if (!mp && s.flags) S1D_CUDA(cudaMemsetAsync(s.big(), 0, sizeof(int), s.st)); // new data: re-arm
             const std::uint64_t wu = cfg.block_width;
             const double* src = host_in + (io.local ? 0 : s.start * spec.vpp);
