@@ -64,7 +64,7 @@ struct Shard {
     cudaEvent_t ev_fin = nullptr;           // final-slice D2H ordering
     cudaStream_t st2 = nullptr;             // second compute stream of the wavefront solve
     std::vector<cudaEvent_t> ev_chunk;      // wavefront solve: [phase slot][chunk] completion
-    cudaEvent_t ev_mid = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_mid = nullptr, ev_join = nullptr, ev_go = nullptr;
     int* err = nullptr;
     double* staging = nullptr; // AoS (vpp = 3) upload/download buffer (Euler)
     const double* final_state = nullptr;
@@ -193,6 +193,7 @@ struct Solver {
             for (cudaEvent_t e : s.ev_chunk) cudaEventDestroy(e);
             if (s.ev_mid) cudaEventDestroy(s.ev_mid);
             if (s.ev_join) cudaEventDestroy(s.ev_join);
+            if (s.ev_go) cudaEventDestroy(s.ev_go);
             if (s.st2) cudaStreamDestroy(s.st2);
             if (s.cs) cudaStreamDestroy(s.cs);
             if (s.st) cudaStreamDestroy(s.st);
@@ -490,6 +491,7 @@ struct Solver {
             if (!s.st2) S1D_CUDA(cudaStreamCreateWithFlags(&s.st2, cudaStreamNonBlocking));
             if (!s.ev_mid) S1D_CUDA(cudaEventCreateWithFlags(&s.ev_mid, cudaEventDisableTiming));
             if (!s.ev_join) S1D_CUDA(cudaEventCreateWithFlags(&s.ev_join, cudaEventDisableTiming));
+            if (!s.ev_go) S1D_CUDA(cudaEventCreateWithFlags(&s.ev_go, cudaEventDisableTiming));
             while (static_cast<int>(s.ev_chunk.size()) < wave_slots * K) {
                 cudaEvent_t e;
                 S1D_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -802,7 +804,17 @@ struct Solver {
     // before it, and the copy-out of chunk k the last phases of the chunks
     // after it. The ring wraps (chunk 0's left neighbour is chunk K-1), so
     // the head wave grows from chunk 0 upwards and finishes the low chunks
-    // last. Multi-shard runs keep the Up/Down-only pipeline.
+    // last. One process per GPU: a shard's end chunks (0 and K-1) read or
+    // overwrite what the ring neighbours' end chunks use, so each waits on
+    // the device for the neighbours' previous phase (the round flags of
+    // sync.cu, one round per phase as before) and each phase signals its
+    // round once all its chunks are issued. Those runs use one stream: the
+    // spinning waits must never hold back work issued before them, and
+    // streams that share a hardware queue would (a wait of phase p in front
+    // of this shard's own signal of phase p-1, mirrored on the neighbour,
+    // deadlocks); an end chunk of phase p is issued only after the whole of
+    // phase p-1 and its signal, so the waits resolve by induction over p.
+    // Single-process multi-shard runs keep the Up/Down-only pipeline.
     // Shape: 16 chunks and enough pipelined Diamonds that their compute
     // covers one copy of the state. A heat Diamond takes ~m/340 of the copy
     // time (m updates per point at ~2.3 T/s against 8 B per point over PCIe
@@ -835,8 +847,9 @@ struct Solver {
     }
     std::int64_t dom_diamonds = 0; // Diamonds inside the dominant-kernel timing window
 
+    bool wave_eligible() const { return locals.size() == 1 && (R() == 1 || mp) && !debug; }
     bool wavefront(std::int64_t cycles) const {
-        return pio && pio->wave && !mp && R() == 1 && locals.size() == 1 && !debug &&
+        return pio && pio->wave && wave_eligible() &&
                cycles >= wave_head + wave_tail + 2 && pio->K >= 3;
     }
 
@@ -867,20 +880,43 @@ struct Solver {
     }
 
     void wavefront_phases(std::int64_t cycles, s1d_stats& stats) {
-        Shard& s = sh(locals[0]);
+        const int me = locals[0];
+        Shard& s = sh(me);
         S1D_CUDA(cudaSetDevice(s.dev));
         const int K = pio->K;
         const std::int64_t tail0 = cycles - wave_tail; // first tail phase
-        const cudaStream_t sts[2] = {s.st, s.st2};
+        const bool xs = mp && R() > 1;                 // neighbour shards in other processes
+        const unsigned S = seq;                        // rounds completed before the Up
+        const cudaStream_t sts[2] = {s.st, xs ? s.st : s.st2};
         auto slot = [&](std::int64_t p) {
             return p <= wave_head ? static_cast<int>(p) : wave_head + 1 + static_cast<int>(p - tail0);
         };
         auto wrap = [&](int c) { return ((c % K) + K) % K; };
+        auto end_chunk = [&](int c) { return xs && (c == 0 || c == K - 1); };
         std::vector<char> done(static_cast<std::size_t>(wave_slots * K), 0);
         auto is_done = [&](std::int64_t p, int c) -> char& {
             return done[static_cast<std::size_t>(slot(p) * K + wrap(c))];
         };
+        auto phase_done = [&](std::int64_t p) {
+            for (int c = 0; c < K; ++c)
+                if (!is_done(p, c)) return false;
+            return true;
+        };
         auto ev = [&](std::int64_t p, int c) { return s.ev_chunk[static_cast<std::size_t>(slot(p) * K + wrap(c))]; };
+        // multi-process: round signal of each pipelined phase once all its
+        // chunks are issued (phases complete in order)
+        std::int64_t next_sig = 0;
+        auto signal_ready = [&] {
+            while (next_sig <= cycles && (next_sig <= wave_head || next_sig >= tail0) && phase_done(next_sig)) {
+                if (xs) {
+                    S1D_CUDA(launch_signal_flags(left_of(me).flags + 1, right_of(me).flags + 0,
+                                                 S + static_cast<unsigned>(next_sig) + 1, s.st));
+                    if (next_sig > 0)
+                        stats.edge_bytes_device += sizeof(double) * cfg.block_width * static_cast<unsigned>(spec.rec);
+                }
+                ++next_sig;
+            }
+        };
         auto issue = [&](std::int64_t p, int c) {
             const cudaStream_t stream = sts[c & 1];
             if (p == tail0) {
@@ -888,19 +924,30 @@ struct Solver {
             } else if (p > 0) {
                 for (int d = -1; d <= 1; ++d) S1D_CUDA(cudaStreamWaitEvent(stream, ev(p - 1, c + d), 0));
             }
+            if (end_chunk(c)) // the neighbours' phase p-1 (for the Up: their previous run) is done
+                S1D_CUDA(launch_wait_flags(s.flags, S + static_cast<unsigned>(p), s.err, round_timeout_ns(), stream));
             chunk_phase(p, cycles, c, stream, stats);
             S1D_CUDA(cudaEventRecord(ev(p, c), stream));
             is_done(p, c) = 1;
+            signal_ready();
         };
-        S1D_CUDA(cudaStreamWaitEvent(s.st2, s.ev_start, 0));
+        // the second stream starts after the run's start
+        S1D_CUDA(cudaEventRecord(s.ev_go, s.st));
+        if (!xs) S1D_CUDA(cudaStreamWaitEvent(s.st2, s.ev_go, 0));
         // head: Up chunk a once its copy is queued; every head Diamond chunk as
-        // soon as its three neighbours of the previous phase are issued
+        // soon as its three neighbours of the previous phase are issued (end
+        // chunks: the whole previous phase)
+        auto ready = [&](std::int64_t p, int c) {
+            if (is_done(p, c)) return false;
+            if (end_chunk(c)) return phase_done(p - 1);
+            return is_done(p - 1, c - 1) && is_done(p - 1, c) && is_done(p - 1, c + 1);
+        };
         auto drain = [&] {
             for (bool progress = true; progress;) {
                 progress = false;
                 for (std::int64_t p = 1; p <= wave_head; ++p)
                     for (int c = 0; c < K; ++c)
-                        if (!is_done(p, c) && is_done(p - 1, c - 1) && is_done(p - 1, c) && is_done(p - 1, c + 1)) {
+                        if (ready(p, c)) {
                             issue(p, c);
                             progress = true;
                         }
@@ -913,21 +960,40 @@ struct Solver {
         drain();
         // middle: whole-shard Diamonds on s.st after every head chunk
         for (int c = 0; c < K; ++c) S1D_CUDA(cudaStreamWaitEvent(s.st, ev(wave_head, c), 0));
+        if (xs) seq = S + static_cast<unsigned>(wave_head) + 1;
         record_all(&Shard::ev_dom0);
         for (std::int64_t j = wave_head + 1; j < tail0; ++j) swept_phase(kDiamond, j, stats);
         record_all(&Shard::ev_dom1);
         dom_diamonds = tail0 - wave_head - 1;
         S1D_CUDA(cudaEventRecord(s.ev_mid, s.st));
-        // tail: Down chunks in order 0..K-1, each after the cone of tail
-        // chunks it needs (depth-first), so the copy-out starts early
+        next_sig = tail0; // the middle phases signalled their own rounds
+        // tail: Down chunks one by one, each after the cone of tail chunks it
+        // needs (depth-first), so the copy-out starts early. Multi-process: an
+        // end chunk past the first tail phase needs that whole phase before
+        // it, so the Down chunks whose cones avoid end chunks go first.
         std::function<void(std::int64_t, int)> need = [&](std::int64_t p, int c) {
+            c = wrap(c);
             if (p < tail0 || is_done(p, c)) return;
+            if (end_chunk(c) && p > tail0)
+                for (int q = 0; q < K; ++q) need(p - 1, q);
             for (int d = -1; d <= 1; ++d) need(p - 1, c + d);
-            issue(p, wrap(c));
+            issue(p, c);
         };
-        for (int c = 0; c < K; ++c) need(cycles, c);
-        S1D_CUDA(cudaEventRecord(s.ev_join, s.st2));
-        S1D_CUDA(cudaStreamWaitEvent(s.st, s.ev_join, 0));
+        std::vector<int> order;
+        if (xs) {
+            const int D = static_cast<int>(cycles - tail0); // tail Diamonds
+            for (int c = D; c <= K - 1 - D; ++c) order.push_back(c);
+            for (int c = 0; c < K; ++c)
+                if (c < D || c > K - 1 - D) order.push_back(c);
+        } else {
+            for (int c = 0; c < K; ++c) order.push_back(c);
+        }
+        for (int c : order) need(cycles, c);
+        if (xs) seq = S + static_cast<unsigned>(cycles) + 1;
+        if (!xs) {
+            S1D_CUDA(cudaEventRecord(s.ev_join, s.st2));
+            S1D_CUDA(cudaStreamWaitEvent(s.st, s.ev_join, 0));
+        }
     }
 
     void advance(s1d_stats* stats_out, s1d_timing* timing_out) {
@@ -1121,7 +1187,7 @@ struct Solver {
         io.local = local_io();
         std::uint64_t min_nb = ~0ull;
         for (int g : locals) min_nb = std::min<std::uint64_t>(min_nb, sh(g).nb);
-        io.wave = set_wave_shape() && !mp && R() == 1 && locals.size() == 1 && cycles >= wave_head + wave_tail + 2 && min_nb >= 3;
+        io.wave = set_wave_shape() && wave_eligible() && cycles >= wave_head + wave_tail + 2 && min_nb >= 3;
         io.K = static_cast<int>(std::min<std::uint64_t>(io.wave ? wave_chunks : 8, min_nb));
         sync_all();
         for (int g : locals) {
