@@ -12,7 +12,9 @@ One bench "step" = one full solve (`s1d_advance`: UpTriangle, Diamonds,
 DownTriangle) of T time steps from the resident initial condition. `value` is
 device-timed (CUDA events inside the library, on the launching streams), the
 max over ranks; `e2e` times the same solve through the C ABI with pinned HOST
-buffers (H2D of the IC, solve, D2H of the state) every step.
+buffers (H2D of the IC, solve, D2H of the state) every step; the library
+overlaps those copies with the first and last phases of the solve, chunk by
+chunk ("wavefront solve").
 
 --impl reference runs the reference's own CPU engine (sweep1d::run, swept,
 WallClock, compiled from source into oracle/_ref) on this host's cores on a
