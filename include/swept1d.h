@@ -169,6 +169,16 @@ int64_t s1d_cycle_advance(uint64_t w, uint64_t h, char* err, size_t errlen); /* 
 int s1d_message_log(const s1d_config* cfg, s1d_message* out, size_t cap, size_t* count, char* err, size_t errlen);
 /* CommStats::per_rank for cfg (transport.cpp:190-196); arrays of cfg->ranks. */
 int s1d_comm_per_rank(const s1d_config* cfg, s1d_rank_stats* out, size_t cap, char* err, size_t errlen);
+
+/* Test hook (no reference counterpart, no CUDA): the issue order of the
+ * wavefront solve that s1d_solve uses to overlap the host copies (DESIGN.md
+ * §12) for `chunks` chunks, `head` / `tail` pipelined Diamonds, `cycles`
+ * swept cycles, one process per GPU or not. `out` receives *count triples
+ * (kind, phase, chunk) up to `cap` triples; kind 0 = chunk launch,
+ * 1 = round signal (multi-process only), 2 = the whole-shard middle
+ * Diamonds. */
+int s1d_debug_wave_schedule(int chunks, int head, int tail, int64_t cycles, int multi_process, int64_t* out,
+                            size_t cap, size_t* count, char* err, size_t errlen);
 /* kind 0 triangle, 1 diamond, 2 down-triangle. Returns the level count (or
  * -status); fills up to cap (substep, lo, hi) triples. */
 int64_t s1d_schedule(int kind, uint64_t w, uint64_t h, int64_t* substep, int64_t* lo, int64_t* hi, size_t cap,

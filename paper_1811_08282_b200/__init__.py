@@ -18,3 +18,4 @@ from .api import (  # noqa: F401
 from .api import DebugResult, RunOptions, run_debug  # noqa: F401
 from .api import calibrate_transport, virtual_time  # noqa: F401
 from .api import MessageLogEntry, RankCommStats, message_log, rank_stats  # noqa: F401
+from .api import wave_schedule  # noqa: F401

@@ -104,6 +104,8 @@ SIGNATURES = {
     "s1d_message_log": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_message), C.c_size_t,
                                   C.POINTER(C.c_size_t)] + _E),
     "s1d_comm_per_rank": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_rank_stats), C.c_size_t] + _E),
+    "s1d_debug_wave_schedule": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int64, C.c_int, C.POINTER(C.c_int64),
+                                          C.c_size_t, C.POINTER(C.c_size_t)] + _E),
     "s1d_calibrate_transport": (C.c_int, [C.c_int, C.c_int, _dp, _dp] + _E),
     "s1d_measure": (C.c_int, [C.POINTER(s1d_config), C.POINTER(s1d_record)] + _E),
     "s1d_csv_header": (C.c_char_p, []),

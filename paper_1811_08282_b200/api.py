@@ -509,6 +509,20 @@ def message_log(cfg: LaunchConfig) -> list:
     return [MessageLogEntry(m.round, m.source, m.dest, m.tag, m.bytes) for m in arr[:n.value]]
 
 
+def wave_schedule(chunks: int, head: int, tail: int, cycles: int, multi_process: bool = False) -> list:
+    """Issue order of the wavefront solve (test hook, host-only):
+    tuples (kind, phase, chunk), kind "chunk" / "signal" / "middle"."""
+    n = C.c_size_t(0)
+    e = _errbuf()
+    _check(lib().s1d_debug_wave_schedule(chunks, head, tail, cycles, int(multi_process), None, 0, C.byref(n), e,
+                                         1024), e)
+    buf = (C.c_int64 * (3 * max(n.value, 1)))()
+    _check(lib().s1d_debug_wave_schedule(chunks, head, tail, cycles, int(multi_process), buf, n.value, C.byref(n), e,
+                                         1024), e)
+    kinds = ("chunk", "signal", "middle")
+    return [(kinds[buf[3 * i]], buf[3 * i + 1], buf[3 * i + 2]) for i in range(n.value)]
+
+
 @dataclass
 class RunOptions:
     """sweep1d::RunOptions subset (inc/debug.hpp:17-24)."""

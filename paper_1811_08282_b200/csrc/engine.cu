@@ -891,104 +891,42 @@ struct Solver {
         auto slot = [&](std::int64_t p) {
             return p <= wave_head ? static_cast<int>(p) : wave_head + 1 + static_cast<int>(p - tail0);
         };
-        auto wrap = [&](int c) { return ((c % K) + K) % K; };
-        auto end_chunk = [&](int c) { return xs && (c == 0 || c == K - 1); };
-        std::vector<char> done(static_cast<std::size_t>(wave_slots * K), 0);
-        auto is_done = [&](std::int64_t p, int c) -> char& {
-            return done[static_cast<std::size_t>(slot(p) * K + wrap(c))];
-        };
-        auto phase_done = [&](std::int64_t p) {
-            for (int c = 0; c < K; ++c)
-                if (!is_done(p, c)) return false;
-            return true;
-        };
-        auto ev = [&](std::int64_t p, int c) { return s.ev_chunk[static_cast<std::size_t>(slot(p) * K + wrap(c))]; };
-        // multi-process: round signal of each pipelined phase once all its
-        // chunks are issued (phases complete in order)
-        std::int64_t next_sig = 0;
-        auto signal_ready = [&] {
-            while (next_sig <= cycles && (next_sig <= wave_head || next_sig >= tail0) && phase_done(next_sig)) {
-                if (xs) {
-                    S1D_CUDA(launch_signal_flags(left_of(me).flags + 1, right_of(me).flags + 0,
-                                                 S + static_cast<unsigned>(next_sig) + 1, s.st));
-                    if (next_sig > 0)
-                        stats.edge_bytes_device += sizeof(double) * cfg.block_width * static_cast<unsigned>(spec.rec);
-                }
-                ++next_sig;
-            }
-        };
-        auto issue = [&](std::int64_t p, int c) {
-            const cudaStream_t stream = sts[c & 1];
-            if (p == tail0) {
-                S1D_CUDA(cudaStreamWaitEvent(stream, s.ev_mid, 0));
-            } else if (p > 0) {
-                for (int d = -1; d <= 1; ++d) S1D_CUDA(cudaStreamWaitEvent(stream, ev(p - 1, c + d), 0));
-            }
-            if (end_chunk(c)) // the neighbours' phase p-1 (for the Up: their previous run) is done
-                S1D_CUDA(launch_wait_flags(s.flags, S + static_cast<unsigned>(p), s.err, round_timeout_ns(), stream));
-            chunk_phase(p, cycles, c, stream, stats);
-            S1D_CUDA(cudaEventRecord(ev(p, c), stream));
-            is_done(p, c) = 1;
-            signal_ready();
+        auto ev = [&](std::int64_t p, int c) {
+            return s.ev_chunk[static_cast<std::size_t>(slot(p) * K + ((c % K) + K) % K)];
         };
         // the second stream starts after the run's start
         S1D_CUDA(cudaEventRecord(s.ev_go, s.st));
         if (!xs) S1D_CUDA(cudaStreamWaitEvent(s.st2, s.ev_go, 0));
-        // head: Up chunk a once its copy is queued; every head Diamond chunk as
-        // soon as its three neighbours of the previous phase are issued (end
-        // chunks: the whole previous phase)
-        auto ready = [&](std::int64_t p, int c) {
-            if (is_done(p, c)) return false;
-            if (end_chunk(c)) return phase_done(p - 1);
-            return is_done(p - 1, c - 1) && is_done(p - 1, c) && is_done(p - 1, c + 1);
-        };
-        auto drain = [&] {
-            for (bool progress = true; progress;) {
-                progress = false;
-                for (std::int64_t p = 1; p <= wave_head; ++p)
-                    for (int c = 0; c < K; ++c)
-                        if (ready(p, c)) {
-                            issue(p, c);
-                            progress = true;
-                        }
+        // issue order and its invariants: host_wave.cpp
+        for (const WaveStep& step : wave_schedule(K, wave_head, wave_tail, cycles, xs)) {
+            const std::int64_t p = step.p;
+            const int c = step.c;
+            if (step.kind == kWaveChunk) {
+                const cudaStream_t stream = sts[c & 1];
+                if (p == tail0) {
+                    S1D_CUDA(cudaStreamWaitEvent(stream, s.ev_mid, 0));
+                } else if (p > 0) {
+                    for (int d = -1; d <= 1; ++d) S1D_CUDA(cudaStreamWaitEvent(stream, ev(p - 1, c + d), 0));
+                }
+                if (xs && (c == 0 || c == K - 1)) // the neighbours' phase p-1 (Up: their previous run) is done
+                    S1D_CUDA(launch_wait_flags(s.flags, S + static_cast<unsigned>(p), s.err, round_timeout_ns(),
+                                               stream));
+                chunk_phase(p, cycles, c, stream, stats);
+                S1D_CUDA(cudaEventRecord(ev(p, c), stream));
+            } else if (step.kind == kWaveSignal) {
+                S1D_CUDA(launch_signal_flags(left_of(me).flags + 1, right_of(me).flags + 0,
+                                             S + static_cast<unsigned>(p) + 1, s.st));
+                if (p > 0) stats.edge_bytes_device += sizeof(double) * cfg.block_width * static_cast<unsigned>(spec.rec);
+            } else { // middle: whole-shard Diamonds on s.st after every head chunk
+                for (int k = 0; k < K; ++k) S1D_CUDA(cudaStreamWaitEvent(s.st, ev(wave_head, k), 0));
+                if (xs) seq = S + static_cast<unsigned>(wave_head) + 1;
+                record_all(&Shard::ev_dom0);
+                for (std::int64_t j = wave_head + 1; j < tail0; ++j) swept_phase(kDiamond, j, stats);
+                record_all(&Shard::ev_dom1);
+                dom_diamonds = tail0 - wave_head - 1;
+                S1D_CUDA(cudaEventRecord(s.ev_mid, s.st));
             }
-        };
-        for (int a = 0; a < K; ++a) {
-            drain();
-            issue(0, a);
         }
-        drain();
-        // middle: whole-shard Diamonds on s.st after every head chunk
-        for (int c = 0; c < K; ++c) S1D_CUDA(cudaStreamWaitEvent(s.st, ev(wave_head, c), 0));
-        if (xs) seq = S + static_cast<unsigned>(wave_head) + 1;
-        record_all(&Shard::ev_dom0);
-        for (std::int64_t j = wave_head + 1; j < tail0; ++j) swept_phase(kDiamond, j, stats);
-        record_all(&Shard::ev_dom1);
-        dom_diamonds = tail0 - wave_head - 1;
-        S1D_CUDA(cudaEventRecord(s.ev_mid, s.st));
-        next_sig = tail0; // the middle phases signalled their own rounds
-        // tail: Down chunks one by one, each after the cone of tail chunks it
-        // needs (depth-first), so the copy-out starts early. Multi-process: an
-        // end chunk past the first tail phase needs that whole phase before
-        // it, so the Down chunks whose cones avoid end chunks go first.
-        std::function<void(std::int64_t, int)> need = [&](std::int64_t p, int c) {
-            c = wrap(c);
-            if (p < tail0 || is_done(p, c)) return;
-            if (end_chunk(c) && p > tail0)
-                for (int q = 0; q < K; ++q) need(p - 1, q);
-            for (int d = -1; d <= 1; ++d) need(p - 1, c + d);
-            issue(p, c);
-        };
-        std::vector<int> order;
-        if (xs) {
-            const int D = static_cast<int>(cycles - tail0); // tail Diamonds
-            for (int c = D; c <= K - 1 - D; ++c) order.push_back(c);
-            for (int c = 0; c < K; ++c)
-                if (c < D || c > K - 1 - D) order.push_back(c);
-        } else {
-            for (int c = 0; c < K; ++c) order.push_back(c);
-        }
-        for (int c : order) need(cycles, c);
         if (xs) seq = S + static_cast<unsigned>(cycles) + 1;
         if (!xs) {
             S1D_CUDA(cudaEventRecord(s.ev_join, s.st2));
@@ -1403,6 +1341,21 @@ int s1d_message_log(const s1d_config* cfg, s1d_message* out, size_t cap, size_t*
         const auto log = s1d::message_log(c);
         *count = log.size();
         for (std::size_t i = 0; i < log.size() && i < cap; ++i) out[i] = log[i];
+    });
+}
+
+int s1d_debug_wave_schedule(int chunks, int head, int tail, int64_t cycles, int multi_process, int64_t* out,
+                            size_t cap, size_t* count, char* err, size_t errlen) {
+    return guarded(err, errlen, [&] {
+        need(count, "count");
+        if (cap && !out) need(out, "out");
+        const auto steps = s1d::wave_schedule(chunks, head, tail, cycles, multi_process != 0);
+        *count = steps.size();
+        for (std::size_t i = 0; i < steps.size() && i < cap; ++i) {
+            out[3 * i] = steps[i].kind;
+            out[3 * i + 1] = steps[i].p;
+            out[3 * i + 2] = steps[i].c;
+        }
     });
 }
 

@@ -65,6 +65,14 @@ double virtual_clock(const s1d_config& cfg, double* comm_seconds);
 // The reference transport's sorted message log and per-rank counters for a
 // config (host_model.cpp).
 std::vector<s1d_message> message_log(const s1d_config& cfg);
+// Wavefront solve issue order (host_wave.cpp).
+enum { kWaveChunk = 0, kWaveSignal = 1, kWaveMiddle = 2 };
+struct WaveStep {
+    int kind;       // kWaveChunk: chunk c of phase p; kWaveSignal: round of phase p; kWaveMiddle
+    std::int64_t p; // phase (0: Up, cycles: Down)
+    int c;          // chunk
+};
+std::vector<WaveStep> wave_schedule(int K, int head, int tail, std::int64_t cycles, bool xs);
 std::vector<s1d_rank_stats> rank_stats(const s1d_config& cfg);
 
 } // namespace s1d
