@@ -271,8 +271,13 @@ inline int euler_tiles_per_cta(int flat, int w) {
 // shared memory; same code, same barriers, same arithmetic.
 // WT > 0: the tile width (and then the CTA size, MAXT) as compile-time
 // constants, so tile offsets fold into immediates (the common widths).
-template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false, int WT = 0>
-__global__ void __launch_bounds__(MAXT, MAXT > 256 ? 1 : S1D_EULER_MINB) euler_tile(const TileArgs a, int GT) {
+// ONE: one tile per CTA (every width above 128) as a compile-time fact, so
+// the multi-tile paths (a division per visited point, per-tile liveness)
+// fold away: measured +9-10% at w = 512.
+template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false, int WT = 0, bool ONE = false>
+__global__ void __launch_bounds__(MAXT, MAXT > 512 ? 1 : MAXT > 256 ? 2 : MAXT > 128 ? S1D_EULER_MINB : 2 * S1D_EULER_MINB)
+    euler_tile(const TileArgs a, int GT) {
+    if (ONE) GT = 1;
     using G = TileGeom<FLAT>;
     constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
     extern __shared__ double sm[];
@@ -551,9 +556,16 @@ cudaError_t launch_tile_f(int kind, const TileArgs& a_in, cudaStream_t st, int c
     const int GT = GMEM ? 1 : euler_tiles_per_cta(FLAT, a.w);
     const std::size_t ring_doubles = 2 * (std::size_t)kERing * TileGeom<FLAT>::LVL;
     const size_t smem = GMEM ? GT * ring_doubles * sizeof(double) : (size_t)GT * euler_tile_smem(FLAT, a.w);
-    void (*k)(const TileArgs, int) = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, GMEM, WT>
-                                     : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, GMEM, WT>
-                                                        : euler_tile<FLAT, kDown, DBG, MAXT, GMEM, WT>;
+    void (*k)(const TileArgs, int) = nullptr;
+    if (GT == 1 || WT || GMEM) {
+        k = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, GMEM, WT, true>
+            : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, GMEM, WT, true>
+                               : euler_tile<FLAT, kDown, DBG, MAXT, GMEM, WT, true>;
+    } else if constexpr (!WT && !GMEM) {
+        k = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, false, 0, false>
+            : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, false, 0, false>
+                               : euler_tile<FLAT, kDown, DBG, MAXT, false, 0, false>;
+    }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
@@ -653,13 +665,20 @@ cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_
     // run 512 threads per CTA: measured +11-14% at w = 1024 (slower at w <= 512).
     const int cap = !wide && (size_t)GT * euler_tile_smem(flat, a.w) > 76 * 1024 ? 512 : 0;
     if (const char* e = std::getenv("S1D_EULER_NT")) wide = std::atoi(e) > 256;
+    // The common widths run builds with the tile width and CTA size as
+    // compile-time constants (w = 256: 128 threads; 512: 256; 1024: 512).
+    const bool fixed = GT == 1 && !std::getenv("S1D_EULER_NT");
+    if (!wide && cap == 512 && fixed && a.w == 1024)
+        return flat ? launch_tile_f<1, false, 512, false, 1024>(kind, a, st)
+                    : launch_tile_f<0, false, 512, false, 1024>(kind, a, st);
     if (wide || cap)
         return flat ? launch_tile_f<1, false, 1024>(kind, a, st, cap) : launch_tile_f<0, false, 1024>(kind, a, st, cap);
-    // w = 512 (the 256-thread build's widest tile): width and CTA size as
-    // compile-time constants (measured: flattening +3%, lengthening +0.5%)
-    if (a.w == 512 && euler_tiles_per_cta(flat, a.w) == 1 && !std::getenv("S1D_EULER_NT"))
+    if (fixed && a.w == 512)
         return flat ? launch_tile_f<1, false, 256, false, 512>(kind, a, st)
                     : launch_tile_f<0, false, 256, false, 512>(kind, a, st);
+    if (fixed && a.w == 256)
+        return flat ? launch_tile_f<1, false, 128, false, 256>(kind, a, st)
+                    : launch_tile_f<0, false, 128, false, 256>(kind, a, st);
     return flat ? launch_tile_f<1>(kind, a, st) : launch_tile_f<0>(kind, a, st);
 }
 
