@@ -273,11 +273,13 @@ inline int euler_tiles_per_cta(int flat, int w) {
 // constants, so tile offsets fold into immediates (the common widths).
 // ONE: one tile per CTA (every width above 128) as a compile-time fact, so
 // the multi-tile paths (a division per visited point, per-tile liveness)
-// fold away: measured +9-10% at w = 512.
-template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false, int WT = 0, bool ONE = false>
+// fold away: measured +9-10% at w = 512. GTC > 0: the tiles per CTA of a
+// narrow fixed-width build as a compile-time constant.
+template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false, int WT = 0, bool ONE = false, int GTC = 0>
 __global__ void __launch_bounds__(MAXT, MAXT > 512 ? 1 : MAXT > 256 ? 2 : MAXT > 128 ? S1D_EULER_MINB : 2 * S1D_EULER_MINB)
     euler_tile(const TileArgs a, int GT) {
     if (ONE) GT = 1;
+    else if (GTC) GT = GTC;
     using G = TileGeom<FLAT>;
     constexpr int H = G::H, REC = G::REC, LVL = G::LVL;
     extern __shared__ double sm[];
@@ -550,21 +552,27 @@ std::size_t smem_optin() {
     return v;
 }
 
-template <int FLAT, bool DBG = false, int MAXT = 256, bool GMEM = false, int WT = 0>
+template <int FLAT, bool DBG = false, int MAXT = 256, bool GMEM = false, int WT = 0, int GTC = 0>
 cudaError_t launch_tile_f(int kind, const TileArgs& a_in, cudaStream_t st, int cap_threads = 0) {
     TileArgs a = a_in;
-    const int GT = GMEM ? 1 : euler_tiles_per_cta(FLAT, a.w);
+    const int GT = GMEM ? 1 : GTC ? GTC : euler_tiles_per_cta(FLAT, a.w);
     const std::size_t ring_doubles = 2 * (std::size_t)kERing * TileGeom<FLAT>::LVL;
     const size_t smem = GMEM ? GT * ring_doubles * sizeof(double) : (size_t)GT * euler_tile_smem(FLAT, a.w);
     void (*k)(const TileArgs, int) = nullptr;
-    if (GT == 1 || WT || GMEM) {
-        k = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, GMEM, WT, true>
-            : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, GMEM, WT, true>
-                               : euler_tile<FLAT, kDown, DBG, MAXT, GMEM, WT, true>;
-    } else if constexpr (!WT && !GMEM) {
-        k = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, false, 0, false>
-            : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, false, 0, false>
-                               : euler_tile<FLAT, kDown, DBG, MAXT, false, 0, false>;
+    if constexpr (GTC > 1) {
+        k = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, false, WT, false, GTC>
+            : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, false, WT, false, GTC>
+                               : euler_tile<FLAT, kDown, DBG, MAXT, false, WT, false, GTC>;
+    } else {
+        if (GT == 1 || WT || GMEM) {
+            k = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, GMEM, WT, true>
+                : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, GMEM, WT, true>
+                                   : euler_tile<FLAT, kDown, DBG, MAXT, GMEM, WT, true>;
+        } else if constexpr (!WT && !GMEM) {
+            k = kind == kUp ? euler_tile<FLAT, kUp, DBG, MAXT, false, 0, false>
+                : kind == kDiamond ? euler_tile<FLAT, kDiamond, DBG, MAXT, false, 0, false>
+                                   : euler_tile<FLAT, kDown, DBG, MAXT, false, 0, false>;
+        }
     }
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -671,6 +679,13 @@ cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_
     if (!wide && cap == 512 && fixed && a.w == 1024)
         return flat ? launch_tile_f<1, false, 512, false, 1024>(kind, a, st)
                     : launch_tile_f<0, false, 512, false, 1024>(kind, a, st);
+    if (!wide && cap == 512 && fixed && a.w == 2048)
+        return flat ? launch_tile_f<1, false, 512, false, 2048>(kind, a, st)
+                    : launch_tile_f<0, false, 512, false, 2048>(kind, a, st);
+    // latency-bound grids at w = 512: one thread per span point, 17 warps
+    if (wide && fixed && a.w == 512)
+        return flat ? launch_tile_f<1, false, 544, false, 512>(kind, a, st)
+                    : launch_tile_f<0, false, 544, false, 512>(kind, a, st);
     if (wide || cap)
         return flat ? launch_tile_f<1, false, 1024>(kind, a, st, cap) : launch_tile_f<0, false, 1024>(kind, a, st, cap);
     if (fixed && a.w == 512)
@@ -679,6 +694,19 @@ cudaError_t launch_euler_tile(int flat, int kind, const TileArgs& a, cudaStream_
     if (fixed && a.w == 256)
         return flat ? launch_tile_f<1, false, 128, false, 256>(kind, a, st)
                     : launch_tile_f<0, false, 128, false, 256>(kind, a, st);
+    // narrow fixed widths: several tiles per 256-thread CTA (GT as measured
+    // by euler_tiles_per_cta, a compile-time constant here)
+    if (!std::getenv("S1D_EULER_NT") && !std::getenv("S1D_EULER_GT")) {
+        if (flat) {
+            if (a.w == 128 && GT == 4) return launch_tile_f<1, false, 256, false, 128, 4>(kind, a, st);
+            if (a.w == 64 && GT == 4) return launch_tile_f<1, false, 256, false, 64, 4>(kind, a, st);
+            if (a.w == 32 && GT == 8) return launch_tile_f<1, false, 256, false, 32, 8>(kind, a, st);
+        } else {
+            if (a.w == 128 && GT == 4) return launch_tile_f<0, false, 256, false, 128, 4>(kind, a, st);
+            if (a.w == 64 && GT == 8) return launch_tile_f<0, false, 256, false, 64, 8>(kind, a, st);
+            if (a.w == 32 && GT == 8) return launch_tile_f<0, false, 256, false, 32, 8>(kind, a, st);
+        }
+    }
     return flat ? launch_tile_f<1>(kind, a, st) : launch_tile_f<0>(kind, a, st);
 }
 
