@@ -304,7 +304,8 @@ __global__ void __launch_bounds__(MAXT, MAXT > 512 ? 1 : MAXT > 256 ? 2 : MAXT >
     bool bad = false;
 
     auto tile_of = [&](int gi) { return a.b0 + (int)blockIdx.x * GT + gi; };
-    auto live = [&](int gi) { return tile_of(gi) < (a.b1 < 0 ? a.nb : a.b1); };
+    // one tile per CTA: the launcher's grid is exactly the tile count
+    auto live = [&](int gi) { return ONE || tile_of(gi) < (a.b1 < 0 ? a.nb : a.b1); };
     auto origin = [&](int gi) { // shard position of local x = 0
         const int b = tile_of(gi);
         const std::int64_t centre = a.seam ? (std::int64_t)(b + 1) * w : (std::int64_t)b * w + w / 2;
