@@ -269,6 +269,14 @@ inline int euler_tiles_per_cta(int flat, int w) {
 // bound, R/core/src/swept.cpp:10-19) keep records, pressures and fluxes in a
 // per-CTA global scratch block (L1/L2-resident) and only the edge ring in
 // shared memory; same code, same barriers, same arithmetic.
+// Resident CTAs the register budget is sized for: 64 registers per thread
+// (2048 / MAXT CTAs, at most 4 of 256), except the w = 128 build (4 tiles per
+// CTA), which measured 4-6% faster at 85 registers and 3 CTAs/SM (w = 64..512
+// were 5-12% slower that way).
+constexpr int euler_min_blocks(int maxt, int wt) {
+    return maxt > 512 ? 1 : maxt > 256 ? 2 : maxt > 128 ? (wt == 128 ? 3 : S1D_EULER_MINB) : 2 * S1D_EULER_MINB;
+}
+
 // WT > 0: the tile width (and then the CTA size, MAXT) as compile-time
 // constants, so tile offsets fold into immediates (the common widths).
 // ONE: one tile per CTA (every width above 128) as a compile-time fact, so
@@ -276,8 +284,7 @@ inline int euler_tiles_per_cta(int flat, int w) {
 // fold away: measured +9-10% at w = 512. GTC > 0: the tiles per CTA of a
 // narrow fixed-width build as a compile-time constant.
 template <int FLAT, int KIND, bool DBG, int MAXT, bool GMEM = false, int WT = 0, bool ONE = false, int GTC = 0>
-__global__ void __launch_bounds__(MAXT, MAXT > 512 ? 1 : MAXT > 256 ? 2 : MAXT > 128 ? S1D_EULER_MINB : 2 * S1D_EULER_MINB)
-    euler_tile(const TileArgs a, int GT) {
+__global__ void __launch_bounds__(MAXT, euler_min_blocks(MAXT, WT)) euler_tile(const TileArgs a, int GT) {
     if (ONE) GT = 1;
     else if (GTC) GT = GTC;
     using G = TileGeom<FLAT>;
