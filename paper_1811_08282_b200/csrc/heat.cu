@@ -369,11 +369,14 @@ __host__ __device__ inline std::size_t fold_smem_doubles(int kind, int w, int P,
 // reads edges only from its own shard and its ring neighbours, whose flags
 // were final when their previous launch completed (the launch waits for it).
 // Without a.big_self the exact build runs ungated.
-template <int Q, int KIND, int MAXT, int MINB, int U, bool XS, bool FU>
+// WT > 0: the tile width as a compile-time constant (then tiles per CTA and
+// every index stride fold into immediates).
+template <int Q, int KIND, int MAXT, int MINB, int U, bool XS, bool FU, int WT = 0>
 __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a, int G) {
     extern __shared__ __align__(16) double sm[];
     if (!FU && a.big_self && ld_flag(a.big_self) == 0) return; // the fast build computed every CTA
-    const int w = a.w, m = a.m;
+    const int w = WT ? WT : a.w, m = WT ? WT / 2 : a.m;
+    if (WT) G = MAXT / ((WT / 2 + Q - 1) / Q);
     const int tt = (m + Q - 1) / Q; // slots per tile (fold_slots)
     const int nt = tt * G;
     const int t = threadIdx.x;
@@ -792,13 +795,14 @@ int tiles_per_cta(int w, int p, int maxt = 256) {
     return G;
 }
 
-template <int P, int MAXT = 256, int MINB = 1, int U = 1, bool XS = false>
+template <int P, int MAXT = 256, int MINB = 1, int U = 1, bool XS = false, int WT = 0>
 cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     static_assert(P % 2 == 0, "the folded layout holds P/2 distance pairs per thread");
     if (XS != (a.m <= kXportLevels)) return cudaErrorInvalidValue;
     const int tt = fold_slots(a.w, P);
     if (tt > MAXT) return cudaErrorInvalidValue;
     const int G = tiles_per_cta(a.w, P, MAXT);
+    if (WT && (a.w != WT || G * tt != MAXT)) return cudaErrorInvalidValue; // the compile-time shape must match
     const int nt = G * tt;
     const size_t smem = sizeof(double) * fold_smem_doubles(kind, a.w, P, G);
     const int count = (a.b1 < 0 ? a.nb : a.b1) - a.b0;
@@ -813,12 +817,12 @@ cudaError_t launch_tile_p(int kind, const TileArgs& a, cudaStream_t st) {
     for (int pass = fast ? 0 : 1; pass < (fast && !a.gated ? 1 : 2); ++pass) {
         const bool fu = pass == 0;
         void (*k)(const TileArgs, int) =
-            kind == kUp ? (fu ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, true>
-                              : heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, false>)
-            : kind == kDiamond ? (fu ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, true>
-                                     : heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, false>)
-                               : (fu ? heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, true>
-                                     : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, false>);
+            kind == kUp ? (fu ? heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, true, WT>
+                              : heat_tile_kernel<P / 2, kUp, MAXT, MINB, U, XS, false, WT>)
+            : kind == kDiamond ? (fu ? heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, true, WT>
+                                     : heat_tile_kernel<P / 2, kDiamond, MAXT, MINB, U, XS, false, WT>)
+                               : (fu ? heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, true, WT>
+                                     : heat_tile_kernel<P / 2, kDown, MAXT, MINB, U, XS, false, WT>);
         if (smem > 48 * 1024) {
             cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
             if (e != cudaSuccess) return e;
@@ -935,6 +939,12 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
         // level wastes half as many lanes. Measured (n = 2^27) against 256-thread
         // CTAs at 4 per SM: w = 256 / 1024 / 2048: 2.27 / 2.17 / 2.14 T vs
         // 2.13 / 2.10 / 2.09 T; 1024-thread CTAs: 1.99 / 2.09 T.
+        // The common widths with the width as a compile-time constant.
+        if (tiles_per_cta(a.w, 16, kWideCta) * fold_slots(a.w, 16) == kWideCta) {
+            if (a.w == 256) return launch_tile_p<16, kWideCta, 2, 2, false, 256>(kind, a, st);
+            if (a.w == 512) return launch_tile_p<16, kWideCta, 2, 2, false, 512>(kind, a, st);
+            if (a.w == 1024) return launch_tile_p<16, kWideCta, 2, 2, false, 1024>(kind, a, st);
+        }
         return launch_tile_p<16, kWideCta, 2, 2>(kind, a, st);
     default: return cudaErrorInvalidValue;
     }
