@@ -303,6 +303,42 @@ __device__ __forceinline__ void fexpand(const Fold<Q>& c, double (&vl)[Q], doubl
     fexpand_seg<Q, U, FU, false, true>(c, vl, vr, e2, r1, fo, feed);
 }
 
+// Expanding levels when a warp holds exactly one slot s (G >= 32 tiles per
+// CTA, Q divides m: the fixed-width builds). Slot s inserts at levels
+// r = sQ + j, j = 0..Q: only distances r-1 and r are new inside the
+// dependency cone (larger ones are out of it and may hold anything, finsert),
+// and with the level loop unrolled over j their registers (j-1, j) are
+// compile-time: four ring loads from two indices instead of finsert's
+// 2·Q predicated loads, each with its own swizzled index.
+template <int Q, int U, bool FU, class Feed>
+__device__ __forceinline__ void fexpand_slot(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
+                                             double fo, Feed& feed) {
+    const int a = c.s * Q;
+    const int e0 = min(max(a, r0), r1), e2 = min(max(a + Q + 1, r0), r1);
+    fexpand_seg<Q, U, FU, false, false>(c, vl, vr, r0, e0, fo, feed);
+#pragma unroll
+    for (int j = 0; j <= Q; ++j) {
+        const int r = a + j;
+        if (r >= e0 && r < e2) { // warp-uniform
+            const int i0 = ridx(2 * r - 2, c.rmask, c.g, c.G), i1 = ridx(2 * r - 1, c.rmask, c.g, c.G);
+            S1D_CHECK(i0 < (c.rmask + 1) * c.G && i1 < (c.rmask + 1) * c.G, c.err);
+            if (j >= 1) { // distance r-1: left at ring index 2r-1, right at 2r-2
+                vl[j >= 1 ? j - 1 : 0] = c.ringR[i1];
+                vr[j >= 1 ? j - 1 : 0] = c.ringL[i0];
+            }
+            if (j < Q) { // distance r: left at 2r-2, right at 2r-1
+                vl[j < Q ? j : 0] = c.ringR[i0];
+                vr[j < Q ? j : 0] = c.ringL[i1];
+            }
+            fpublish(c, vl, vr, r);
+            feed(r);
+            level_sync();
+            if (j >= 1) fcompute<Q, FU>(c, vl, vr, r, fo); // compute from sQ+1
+        }
+    }
+    fexpand_seg<Q, U, FU, false, true>(c, vl, vr, e2, r1, fo, feed);
+}
+
 template <int Q, int U, bool FU, bool PB, bool CP, bool EX>
 __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                               double fo, double* oL, double* oR, bool live) {
@@ -515,7 +551,10 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     double* oR = a.out_R + (std::size_t)b * w;
 
     if (KIND != kUp) {
-        fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
+        // one slot per warp (compile-time: the fixed-width builds)
+        constexpr bool kSlotWarp = WT > 0 && (WT / 2) % Q == 0 && MAXT / ((WT / 2) / Q) >= 32;
+        if constexpr (kSlotWarp) fexpand_slot<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
+        else fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
         { // level m: full span; the halo pair (x = 0, w+1) is distance m
             const int r = m;
             finsert(c, vl, vr, r);
