@@ -816,23 +816,23 @@ struct Solver {
     // phase p-1 and its signal, so the waits resolve by induction over p.
     // Single-process multi-shard runs keep the Up/Down-only pipeline.
     // Shape: 16 chunks and enough pipelined Diamonds that their compute
-    // covers one copy of the state. A heat Diamond takes ~m/340 of the copy
-    // time (m updates per point at ~2.3 T/s against 8 B per point over PCIe
-    // at ~55 GB/s), so ceil(256/m) Diamonds plus the Up: 2 at the bench's
-    // m = 128 (the best of 1..6 measured there: 370 ms against 390 ms for the
-    // Up/Down-only pipeline). Where one Diamond would do (heat m >= 256, and
-    // Euler, whose updates cost ~100x more) the Up and Down already hide most
-    // of the copies and the chunked Diamonds cost more than they save
-    // (measured: even at m = 512, 4% slower for Euler at w = 512), so those
-    // keep the Up/Down-only pipeline. S1D_WAVE = "chunks,head,tail" forces a
-    // shape (development knob). Returns whether to use the wavefront.
+    // covers one copy of the state: a heat Diamond takes ~m/420 of the copy
+    // time (m updates per point at ~2.9 T/s against 8 B per point over PCIe
+    // at ~55 GB/s), so ceil(384/m) Diamonds plus the Up: 3 at the bench's
+    // m = 128 (measured 300.9 ms per solve against 303.0 with 2 and 301.1-
+    // 301.6 with 4-5; the Up/Down-only pipeline took 31 ms more), 1 at m = 512
+    // (368.5 against 370.0 ms). Euler keeps the Up/Down-only pipeline: its
+    // copies are small against its compute and the chunked Diamonds' partial
+    // waves cost more than they hide (measured 4% slower at w = 512).
+    // S1D_WAVE = "chunks,head,tail" forces a shape (development knob).
+    // Returns whether to use the wavefront.
     int wave_head = 0, wave_tail = 0, wave_slots = 0, wave_chunks = 16;
     bool set_wave_shape() {
         const int mm = static_cast<int>(m);
-        wave_head = euler ? 1 : std::min(6, std::max(1, (256 + mm - 1) / mm));
+        wave_head = euler ? 1 : std::min(6, std::max(1, (384 + mm - 1) / mm));
         wave_tail = wave_head;
         wave_chunks = 16;
-        bool use = wave_head >= 2;
+        bool use = !euler;
         if (const char* e = std::getenv("S1D_WAVE")) {
             int k = 0, h = 0, t = 0;
             if (std::sscanf(e, "%d,%d,%d", &k, &h, &t) == 3 && k >= 3 && h >= 0 && t >= 0) {

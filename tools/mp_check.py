@@ -34,7 +34,7 @@ CASES = [
 WAVE_CASES = [
     # equation, method, n, w, steps, S1D_WAVE shape (96 tiles: >= 12 per rank up to 8 ranks)
     ("heat", "lengthening", 96 * 64, 64, 32 * 9, "16,3,3"),
-    ("heat", "lengthening", 96 * 256, 256, 128 * 7, None),
+    ("heat", "lengthening", 96 * 256, 256, 128 * 9, None),
     ("heat", "lengthening", 96 * 64, 64, 32 * 10, "5,1,2"),
     ("euler", "lengthening", 96 * 64, 64, 72, "16,2,2"),
     ("euler", "flattening", 96 * 64, 64, 80, "7,1,1"),
@@ -108,8 +108,8 @@ def main():
     # >= 2^1022 near rank 0's right seam flags rank 0's Up; the flag spreads
     # to the neighbours' launches through the IPC-shared flag words, the gated
     # exact builds recompute, and the result is the oracle's, bit for bit
-    # (T = 700: classic pad, Up/Down pipeline; T = 896: 7 cycles, wavefront)
-    for T in (700, 896):
+    # (T = 700: classic pad, Up/Down pipeline; T = 1152: 9 cycles, wavefront)
+    for T in (700, 1152):
         n, w = 96 * 256, 256
         cfg = s1d.LaunchConfig(equation=s1d.Equation.Heat, scheme=s1d.Scheme.Swept, grid_size=n, block_width=w,
                                ranks=world, steps=T)
