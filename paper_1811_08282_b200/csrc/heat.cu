@@ -339,6 +339,46 @@ __device__ __forceinline__ void fexpand_slot(const Fold<Q>& c, double (&vl)[Q], 
     fexpand_seg<Q, U, FU, false, true>(c, vl, vr, e2, r1, fo, feed);
 }
 
+// The same when a warp holds NS > 1 consecutive slots (G = 32/NS tiles per
+// CTA): the warp's insert levels are r = saQ + jw, jw = 0..NS·Q, and a lane
+// of slot sa+q fills registers jw-qQ-1 and jw-qQ, compile-time for each q,
+// chosen by the lane's q at run time (one predicated move per candidate).
+template <int Q, int U, bool FU, int NS, class Feed>
+__device__ __forceinline__ void fexpand_slots(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
+                                              double fo, Feed& feed) {
+    const int a = c.sa * Q, q = c.s - c.sa;
+    const int e0 = min(max(a, r0), r1), e1 = min(max(a + 1, r0), r1), e2 = min(max(a + NS * Q + 1, r0), r1);
+    fexpand_seg<Q, U, FU, false, false>(c, vl, vr, r0, e0, fo, feed);
+#pragma unroll
+    for (int jw = 0; jw <= NS * Q; ++jw) {
+        const int r = a + jw;
+        if (r >= e0 && r < e2) { // warp-uniform
+            const int i0 = ridx(2 * r - 2, c.rmask, c.g, c.G), i1 = ridx(2 * r - 1, c.rmask, c.g, c.G);
+            const double l1 = c.ringR[i1], r0v = c.ringL[i0], l0 = c.ringR[i0], r1v = c.ringL[i1];
+#pragma unroll
+            for (int qq = 0; qq < NS; ++qq) {
+                constexpr int kQ = Q;
+                const int j = jw - qq * kQ;
+                if (q == qq) {
+                    if (j >= 1 && j <= kQ) { // distance r-1
+                        vl[(j >= 1 && j <= kQ) ? j - 1 : 0] = l1;
+                        vr[(j >= 1 && j <= kQ) ? j - 1 : 0] = r0v;
+                    }
+                    if (j >= 0 && j < kQ) { // distance r
+                        vl[(j >= 0 && j < kQ) ? j : 0] = l0;
+                        vr[(j >= 0 && j < kQ) ? j : 0] = r1v;
+                    }
+                }
+            }
+            fpublish(c, vl, vr, r);
+            feed(r);
+            level_sync();
+            if (r >= e1) fcompute<Q, FU>(c, vl, vr, r, fo);
+        }
+    }
+    fexpand_seg<Q, U, FU, false, true>(c, vl, vr, e2, r1, fo, feed);
+}
+
 template <int Q, int U, bool FU, bool PB, bool CP, bool EX>
 __device__ __forceinline__ void fcontract_seg(const Fold<Q>& c, double (&vl)[Q], double (&vr)[Q], int r0, int r1,
                                               double fo, double* oL, double* oR, bool live) {
@@ -552,8 +592,11 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
 
     if (KIND != kUp) {
         // one slot per warp (compile-time: the fixed-width builds)
-        constexpr bool kSlotWarp = WT > 0 && (WT / 2) % Q == 0 && MAXT / ((WT / 2) / Q) >= 32;
-        if constexpr (kSlotWarp) fexpand_slot<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
+        constexpr int kG = WT > 0 && (WT / 2) % Q == 0 ? MAXT / ((WT / 2) / Q) : 0; // tiles per CTA
+        if constexpr (kG >= 32) fexpand_slot<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
+#ifndef S1D_HEAT_NO_SLOTS
+        else if constexpr (kG == 16 || kG == 8) fexpand_slots<Q, U, FU, 32 / kG>(c, vl, vr, 1, m, fo, feed);
+#endif
         else fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
         { // level m: full span; the halo pair (x = 0, w+1) is distance m
             const int r = m;
@@ -968,10 +1011,16 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     case 4: // (w = 32: register caps / unroll measured slower)
         return xs ? launch_tile_p<4, 256, 1, 1, true>(kind, a, st) : launch_tile_p<4>(kind, a, st);
     case 8: // measured (w = 64 and widths 16 does not divide): 64-register cap (4 CTAs/SM) + unroll 2
+        if (a.w == 32 && tiles_per_cta(32, 8, 256) * fold_slots(32, 8) == 256)
+            return launch_tile_p<8, 256, 1, 2, true, 32>(kind, a, st); // fixed width
         if (a.w < 64) return launch_tile_p<8, 256, 1, 2, true>(kind, a, st); // w = 32: unroll only
+        if (a.w == 64 && xs && tiles_per_cta(64, 8, 256) * fold_slots(64, 8) == 256)
+            return launch_tile_p<8, 256, 4, 2, true, 64>(kind, a, st); // fixed width
         return xs ? launch_tile_p<8, 256, 4, 2, true>(kind, a, st) : launch_tile_p<8, 256, 4, 2>(kind, a, st);
     case 16: // measured (n = 2^27): 4 CTAs/SM + unroll 2 from w = 256 (1.95-1.97 T), 3 CTAs/SM at w = 128
         if (xs) return launch_tile_p<16, 256, 1, 1, true>(kind, a, st);
+        if (a.w == 128 && tiles_per_cta(128, 16, 256) * fold_slots(128, 16) == 256)
+            return launch_tile_p<16, 256, 3, 1, false, 128>(kind, a, st); // fixed width
         if (a.w < 256) return launch_tile_p<16, 256, 3, 1>(kind, a, st);
         // 512-thread CTAs (2 per SM, 64 registers): twice the tiles per CTA, so
         // a warp spans half the distances and the busy/idle boundary of each
