@@ -3,9 +3,11 @@
 
 Metric: BASELINE.json `metric` (point-updates/s, swept vs classic), on the
 configuration it is quoted on that fits one GPU: configs[1] = heat FP64,
-n = 2^27 per GPU, block width 256 (the fastest width of the 32–1024 sweep at
-this n, profiles/r02_sweep_report.txt — the reference's best-config
-reporting), T = 6144 time steps per run (the paper's ~6000, a multiple of
+n = 2^27 per GPU, block width 1024 (the block-size sweep 32–1024 puts w = 256,
+512 and 1024 within 0.5% of each other at this n, profiles/r02h_heat_report.txt;
+at the bench's T, w = 1024 is the fastest both on the device, 2.874 vs 2.863 T,
+and end to end, 2.79 vs 2.74 T — the reference's best-config reporting),
+T = 6144 time steps per run (the paper's ~6000, a multiple of
 every m = w/2 <= 512 so no classic pad is timed).
 
 One bench "step" = one full solve (`s1d_advance`: UpTriangle, Diamonds,
@@ -504,7 +506,7 @@ def main(argv=None):
     ap.add_argument("--equation", choices=["heat"], default="heat")
     ap.add_argument("--scheme", choices=["swept", "classic"], default="swept")
     ap.add_argument("--log2n", type=int, default=27)
-    ap.add_argument("--w", type=int, default=256, help="block width (the sweep's best at n = 2^27)")
+    ap.add_argument("--w", type=int, default=1024, help="block width (the sweep's best at n = 2^27, T = 6144)")
     ap.add_argument("--T", type=int, default=6144)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--classic-T", type=int, default=256)
