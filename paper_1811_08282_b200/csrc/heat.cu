@@ -940,8 +940,11 @@ int heat_points_per_thread(int w, long long tiles) {
     if (fold_slots(w, p) > 1024) return -1; // no valid decomposition (caller reports it)
     // Small grids: P = 16 packs twice the tiles per CTA of P = 8; below one
     // full wave (4 CTAs per SM) P = 8 fills the GPU better (measured n = 2^20:
-    // 1.29-1.32 T with P = 8 vs 1.01-1.04 T with P = 16 at w = 256..1024).
-    if (p == 16 && tiles >= 0 && fold_slots(w, 8) <= 256) {
+    // 1.29-1.32 T with P = 8 vs 1.01-1.04 T with P = 16 at w = 256..1024) —
+    // except for the fixed-width P = 16 builds (w = 256 / 512 / 1024), which
+    // win there too (n = 2^20: 1.70-1.73 T vs 1.47-1.52 T with P = 8).
+    const bool fixed16 = w == 256 || w == 512 || w == 1024;
+    if (p == 16 && !fixed16 && tiles >= 0 && fold_slots(w, 8) <= 256) {
         static int sms = 0;
         if (sms == 0) {
             int dev = 0;
