@@ -4,7 +4,7 @@
 Metric: BASELINE.json `metric` (point-updates/s, swept vs classic), on the
 configuration it is quoted on that fits one GPU: configs[1] = heat FP64,
 n = 2^27 per GPU, block width 1024 (the block-size sweep 32–1024 puts w = 256,
-512 and 1024 within 0.5% of each other at this n, profiles/r02h_heat_report.txt;
+512 and 1024 within 0.5% of each other at this n, profiles/r02j_heat_report.txt;
 at the bench's T, w = 1024 is the fastest both on the device, 2.874 vs 2.863 T,
 and end to end, 2.79 vs 2.74 T — the reference's best-config reporting),
 T = 6144 time steps per run (the paper's ~6000, a multiple of
