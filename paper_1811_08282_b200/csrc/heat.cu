@@ -591,7 +591,9 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
     double* oR = a.out_R + (std::size_t)b * w;
 
     if (KIND != kUp) {
-        // one slot per warp (compile-time: the fixed-width builds)
+        // Fixed-width builds: one slot per warp (G >= 32 tiles per CTA) or 2 /
+        // 4 slots per warp (G = 16 / 8) insert through the unrolled loops;
+        // the generic builds (and -DS1D_HEAT_NO_SLOTS, a diagnostic) use finsert.
         constexpr int kG = WT > 0 && (WT / 2) % Q == 0 ? MAXT / ((WT / 2) / Q) : 0; // tiles per CTA
         if constexpr (kG >= 32) fexpand_slot<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
 #ifndef S1D_HEAT_NO_SLOTS
