@@ -597,7 +597,7 @@ __global__ void __launch_bounds__(MAXT, MINB) heat_tile_kernel(const TileArgs a,
         constexpr int kG = WT > 0 && (WT / 2) % Q == 0 ? MAXT / ((WT / 2) / Q) : 0; // tiles per CTA
         if constexpr (kG >= 32) fexpand_slot<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
 #ifndef S1D_HEAT_NO_SLOTS
-        else if constexpr (kG == 16 || kG == 8) fexpand_slots<Q, U, FU, 32 / kG>(c, vl, vr, 1, m, fo, feed);
+        else if constexpr (kG == 16 || kG == 8 || kG == 4) fexpand_slots<Q, U, FU, 32 / kG>(c, vl, vr, 1, m, fo, feed);
 #endif
         else fexpand<Q, U, FU>(c, vl, vr, 1, m, fo, feed);
         { // level m: full span; the halo pair (x = 0, w+1) is distance m
@@ -1037,6 +1037,7 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
             if (a.w == 256) return launch_tile_p<16, kWideCta, 2, 2, false, 256>(kind, a, st);
             if (a.w == 512) return launch_tile_p<16, kWideCta, 2, 2, false, 512>(kind, a, st);
             if (a.w == 1024) return launch_tile_p<16, kWideCta, 2, 2, false, 1024>(kind, a, st);
+            if (a.w == 2048) return launch_tile_p<16, kWideCta, 2, 2, false, 2048>(kind, a, st);
         }
         return launch_tile_p<16, kWideCta, 2, 2>(kind, a, st);
     default: return cudaErrorInvalidValue;
