@@ -1017,7 +1017,7 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
         return xs ? launch_tile_p<4, 256, 1, 1, true>(kind, a, st) : launch_tile_p<4>(kind, a, st);
     case 8: // measured (w = 64 and widths 16 does not divide): 64-register cap (4 CTAs/SM) + unroll 2
         if (a.w == 32 && tiles_per_cta(32, 8, 256) * fold_slots(32, 8) == 256)
-            return launch_tile_p<8, 256, 1, 2, true, 32>(kind, a, st); // fixed width
+            return launch_tile_p<8, 256, 4, 2, true, 32>(kind, a, st); // fixed width (64 registers: +16-18%)
         if (a.w < 64) return launch_tile_p<8, 256, 1, 2, true>(kind, a, st); // w = 32: unroll only
         if (a.w == 64 && xs && tiles_per_cta(64, 8, 256) * fold_slots(64, 8) == 256)
             return launch_tile_p<8, 256, 4, 2, true, 64>(kind, a, st); // fixed width
@@ -1025,7 +1025,7 @@ cudaError_t launch_heat_tile(int kind, const TileArgs& a, cudaStream_t st, bool 
     case 16: // measured (n = 2^27): 4 CTAs/SM + unroll 2 from w = 256 (1.95-1.97 T), 3 CTAs/SM at w = 128
         if (xs) return launch_tile_p<16, 256, 1, 1, true>(kind, a, st);
         if (a.w == 128 && tiles_per_cta(128, 16, 256) * fold_slots(128, 16) == 256)
-            return launch_tile_p<16, 256, 3, 1, false, 128>(kind, a, st); // fixed width
+            return launch_tile_p<16, 256, 3, 2, false, 128>(kind, a, st); // fixed width (unroll 2: +2%)
         if (a.w < 256) return launch_tile_p<16, 256, 3, 1>(kind, a, st);
         // 512-thread CTAs (2 per SM, 64 registers): twice the tiles per CTA, so
         // a warp spans half the distances and the busy/idle boundary of each
